@@ -1,0 +1,167 @@
+/*
+ * market_eq_b200 — C ABI of the B200-native PDHCG hot path.
+ *
+ * Drop-in boundary for the reference's fused iteration kernel
+ * (/root/reference/pkg/src/market_eq/kernels.py:99-145, called from
+ * driver._CompactRun.run_chunk, driver.py:134-145) plus the device-side
+ * reductions the reference's solve loop runs between chunks (kkt.py:29-87,
+ * driver.py:123-132, 156-162) and the Arrow-Debreu budget map
+ * (exchange.py:75-93 -> sparse.py:147-153).
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer unless the parameter name ends in
+ *    `_host`.  Buffers are owned by the caller (PyTorch in the Python
+ *    package); the library allocates nothing that outlives a call.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*)
+ *    and graph-capturable, except mq_pdhcg_chunk, which mirrors the
+ *    reference's synchronous return of (navg, faults).
+ *  - Return value: 0 on success, < 0 on a CUDA error (mq_last_error() has the
+ *    message), > 0 only from mq_pdhcg_chunk (= number of faulted rows, which
+ *    the caller turns into SubproblemError exactly as driver.py:142-144).
+ *  - No C++ exception crosses this boundary.
+ *  - Index layout: row offsets int64 [n+1]; column indices int32 [nnz];
+ *    transpose schedule tperm int32 [nnz] / tptr int64 [m+1] (the stable
+ *    column grouping of sparse.py:130-145); values float64.
+ */
+#ifndef MARKET_EQ_B200_H
+#define MARKET_EQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MQ_ABI_VERSION 1
+#define MQ_NBINS 9 /* row-length bins of the fast primal kernel */
+
+/* Read-only market description (device pointers, borrowed). */
+typedef struct mq_market {
+    int64_t n, m, nnz;
+    const int64_t *row_ptr;  /* [n+1]                                          */
+    const int32_t *col;      /* [nnz] strictly increasing within a row         */
+    const double *u;         /* [nnz] normalized utilities (row max 1),
+                                instance.py:118-138                             */
+    const double *u_orig;    /* [nnz] original utilities (residuals, kkt.py)    */
+    const double *w;         /* [n] budgets                                     */
+    const int64_t *tptr;     /* [m+1] column offsets of the transpose schedule  */
+    const int32_t *tperm;    /* [nnz] storage positions grouped by column       */
+    const int32_t *bin_rows; /* [n] row ids grouped by length bin (fast path)   */
+    int64_t bin_off[MQ_NBINS + 1]; /* host-side offsets into bin_rows          */
+    int64_t row_begin;       /* first global row of this shard (0 on 1 GPU)    */
+} mq_market;
+
+/* Mutable iterate of the fast (graph-captured) path.  cs / cs_prev / csbar are
+ * the column sums of x^k, x^{k-1} and xbar: the price step of kernels.py:111-116
+ * needs colsum(2x^k - x^{k-1}) = 2 cs - cs_prev, so x^{k-1} itself is never
+ * stored. */
+typedef struct mq_state {
+    double *x;        /* [nnz] current allocation x^k (updated in place)      */
+    double *xbar;     /* [nnz] running average                                 */
+    double *p;        /* [m]   prices                                          */
+    double *pbar;     /* [m]   running average of prices                       */
+    double *cs;       /* [m]   colsum(x^k)                                     */
+    double *cs_prev;  /* [m]   colsum(x^{k-1})                                 */
+    double *csbar;    /* [m]   colsum(xbar)                                    */
+    const double *steps; /* [2] tau, sigma (device-resident: one graph serves
+                            every step size)                                   */
+    int64_t *navg;    /* [1]  inner iterations since the last restart          */
+    int64_t *pass_out;/* [iters] per-iteration row-solver work counter         */
+    int64_t *faults;  /* [1]  rows whose solver failed                         */
+} mq_state;
+
+/* ---- faithful drop-in ------------------------------------------------------
+ * Replaces kernels.pdhcg_chunk (kernels.py:99-145) argument for argument:
+ * same in-place semantics for x, x_prev, p, xbar, pbar, c_buf and
+ * pass_out[iters]; the literal k-section row search of _row_root
+ * (kernels.py:33-96) with `sections` and `subtol`; fixed-order serial sums.
+ * Bit-identical to the reference on the same inputs.  Synchronous: returns the
+ * fault count (>= 0) and writes the new navg to *navg_out_host. */
+int mq_pdhcg_chunk(int64_t n, int64_t m, const int64_t *indptr, const int32_t *colind,
+                   const double *uval, const int32_t *tperm, const int64_t *tindptr,
+                   const double *w, double *x, double *x_prev, double *p, double *xbar,
+                   double *pbar, int64_t navg, double tau, double sigma, int sections,
+                   double subtol, int iters, double *c_buf, int64_t *pass_out,
+                   int64_t *navg_out_host, void *stream);
+
+/* ---- fast path: one PDHCG iteration as three graph-capturable launches ----
+ * it = index of the iteration inside the chunk (count = *navg + it + 1). */
+
+/* Price step + price average (kernels.py:111-116, 143-144):
+ * p += sigma (2 cs - cs_prev - 1); pbar <- avg; cs_prev <- cs. */
+int mq_dual_step(const mq_market *mk, const mq_state *st, int it, void *stream);
+
+/* Exact per-buyer proximal step fused with the allocation average
+ * (kernels.py:117-142): for every row, the unique root s of
+ * s = sum_j u_j max(0, c_j + tau w u_j / s), c = x - tau p[col], by the
+ * monotone active-set iteration (closed-form root per active set), then
+ * x <- max(0, c + tau w u / s), xbar <- avg.  x_prev_out (may be NULL)
+ * receives the pre-step x (the reference's x_prev copy).
+ * pass_out[it] += number of active-set sweeps. */
+int mq_primal_step(const mq_market *mk, const mq_state *st, int it, double *x_prev_out,
+                   void *stream);
+
+/* cs <- colsum(x) over this shard's rows in the fixed ascending-row order of
+ * the transpose schedule (deterministic, no atomics).  With finalize != 0
+ * (single GPU) also csbar <- avg(csbar, cs); multi-GPU callers allreduce cs
+ * first and then call mq_colsum_finalize. */
+int mq_colsum_step(const mq_market *mk, const mq_state *st, int it, int finalize,
+                   void *stream);
+int mq_colsum_finalize(const mq_market *mk, const mq_state *st, int it, void *stream);
+
+/* navg += iters (end of a captured chunk). */
+int mq_chunk_end(const mq_state *st, int iters, void *stream);
+
+/* Whole chunk on one GPU: `iters` x (dual, primal, colsum) + chunk_end. */
+int mq_fast_chunk(const mq_market *mk, const mq_state *st, int iters, void *stream);
+
+/* Plain column sums out[j] = sum_{col j} v (fixed order), e.g. colsum(x0). */
+int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream);
+
+/* ---- residuals (kkt.py:29-87 specialised to the compact state) -----------
+ * Row pass over this shard: t_i = u_orig_i . x_i, y_i = w_i / t_i, column
+ * maxima colbest_j = max_i u_orig_ij y_i (order-free max, deterministic),
+ * and the entry-wise gap maxima.  `use_norm` selects the normalized
+ * utilities instead (driver.py:123-132 omega_0 norms).
+ * row_out[8] (device): [0] max y, [1] gap numerator max x (p-uy)_+,
+ * [2] max |x|, [3] max (p-uy)_+, [4] first row with t <= 0 (as double, or -1),
+ * [5] sum_i w_i log t_i (fixed order), [6] rows with t <= 0, [7] unused.
+ * t_out / y_out (may be NULL) receive t and y per local row.
+ * colbest must be zero-initialised by the caller (values are positive). */
+int mq_resid_rows(const mq_market *mk, const double *x, const double *p, int use_norm,
+                  double *colbest, double *t_out, double *y_out, double *row_out,
+                  double *scratch, void *stream);
+/* Column pass (replicated data): col_out[6] (device):
+ * [0] max |cs - 1|, [1] max |cs|, [2] max (colbest - p)_+, [3] max (p - colbest)
+ * (initial 0), [4] sum (cs - 1)^2, [5] sum min(p - colbest, 0)^2. */
+int mq_resid_cols(int64_t m, const double *cs, const double *p, const double *colbest,
+                  double *col_out, double *scratch, void *stream);
+
+/* Restart moves (driver.py:156-162): out[4] (device):
+ * [0] sum (xbar-x0)^2 over this shard, [1] sum (pbar-p0)^2,
+ * [2] sum_j (csbar-cs0)_j (pbar-p0)_j, [3] unused. */
+int mq_restart_moves(const mq_market *mk, const double *xbar, const double *x0,
+                     const double *pbar, const double *p0, const double *csbar,
+                     const double *cs0, double *out, double *scratch, void *stream);
+
+/* Sparse matrix-vector product out = E p for a CSR matrix (Arrow-Debreu
+ * budget map, exchange.py:89 -> sparse.py:147-153); fixed-order row sums. */
+int mq_spmv(int64_t n_rows, const int64_t *row_ptr, const int32_t *col,
+            const double *val, const double *v, double *out, void *stream);
+
+/* Row normalization (instance.py:118-138): scales_i = max_j u_ij,
+ * u_out = u / scales_i (IEEE division, bit-identical to the reference). */
+int mq_normalize_rows(int64_t n, const int64_t *row_ptr, const double *u, double *u_out,
+                      double *scales, void *stream);
+
+/* Size in doubles of the `scratch` buffer the reduction calls need. */
+int64_t mq_scratch_doubles(void);
+
+const char *mq_last_error(void);
+int mq_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MARKET_EQ_B200_H */

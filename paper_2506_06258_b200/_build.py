@@ -1,0 +1,64 @@
+"""Build libmarket_eq_b200.so in-tree for sm_100a (nvcc, no torch headers).
+
+    python -m paper_2506_06258_b200._build [--verbose]
+
+The k-section drop-in (ksection.cu) is compiled with --fmad=false so its
+arithmetic rounds exactly like the reference's; the fast path may contract.
+"""
+
+import os
+import subprocess
+import sys
+import tempfile
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIB = os.path.join(PKG, "libmarket_eq_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
+          "--expt-relaxed-constexpr"]
+SOURCES = {
+    "abi.cu": [],
+    "fast.cu": [],
+    "reduce.cu": [],
+    "ksection.cu": ["--fmad=false"],
+}
+
+
+def _sources_newer_than_lib():
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps.append(os.path.join(INCLUDE, "market_eq_b200.h"))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force=False, verbose=False):
+    if not force and not _sources_newer_than_lib():
+        return LIB
+    with tempfile.TemporaryDirectory() as tmp:
+        objs = []
+        for src, extra in SOURCES.items():
+            obj = os.path.join(tmp, src + ".o")
+            cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+            if verbose:
+                cmd += ["-Xptxas", "-v"]
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True)
+            objs.append(obj)
+        tmp_lib = os.path.join(tmp, "lib.so")
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", tmp_lib, *objs,
+               "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
+        subprocess.run(cmd, check=True)
+        os.replace(tmp_lib, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force=True, verbose="--verbose" in sys.argv)
+    print(LIB)

@@ -1,0 +1,111 @@
+"""ctypes binding of libmarket_eq_b200.so (include/market_eq_b200.h).
+
+There is no CPU fallback: importing the solver on a machine without the
+built library or without a CUDA device raises NativeUnavailable the moment a
+device operation is requested.
+"""
+
+import ctypes
+import os
+import threading
+
+from .errors import MarketError
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmarket_eq_b200.so")
+NBINS = 9
+ABI_VERSION = 1
+
+_lock = threading.Lock()
+_lib = None
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+F64 = ctypes.c_double
+CINT = ctypes.c_int
+
+
+class NativeUnavailable(MarketError, RuntimeError):
+    """The sm_100a library or a CUDA device is missing (no CPU fallback)."""
+
+
+class NativeError(MarketError, RuntimeError):
+    """A CUDA call inside the native library failed."""
+
+
+class MqMarket(ctypes.Structure):
+    _fields_ = [("n", I64), ("m", I64), ("nnz", I64),
+                ("row_ptr", P), ("col", P), ("u", P), ("u_orig", P), ("w", P),
+                ("tptr", P), ("tperm", P), ("bin_rows", P),
+                ("bin_off", I64 * (NBINS + 1)), ("row_begin", I64)]
+
+
+class MqState(ctypes.Structure):
+    _fields_ = [("x", P), ("xbar", P), ("p", P), ("pbar", P), ("cs", P), ("cs_prev", P),
+                ("csbar", P), ("steps", P), ("navg", P), ("pass_out", P), ("faults", P)]
+
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "mq_pdhcg_chunk": (CINT, [I64, I64, P, P, P, P, P, P, P, P, P, P, P, I64, F64, F64, CINT,
+                              F64, CINT, P, P, P, P]),
+    "mq_dual_step": (CINT, [P, P, CINT, P]),
+    "mq_primal_step": (CINT, [P, P, CINT, P, P]),
+    "mq_colsum_step": (CINT, [P, P, CINT, CINT, P]),
+    "mq_colsum_finalize": (CINT, [P, P, CINT, P]),
+    "mq_chunk_end": (CINT, [P, CINT, P]),
+    "mq_fast_chunk": (CINT, [P, P, CINT, P]),
+    "mq_colsum": (CINT, [P, P, P, P]),
+    "mq_resid_rows": (CINT, [P, P, P, CINT, P, P, P, P, P, P]),
+    "mq_resid_cols": (CINT, [I64, P, P, P, P, P, P]),
+    "mq_restart_moves": (CINT, [P, P, P, P, P, P, P, P, P, P]),
+    "mq_spmv": (CINT, [I64, P, P, P, P, P, P]),
+    "mq_normalize_rows": (CINT, [I64, P, P, P, P, P]),
+    "mq_scratch_doubles": (I64, []),
+    "mq_last_error": (ctypes.c_char_p, []),
+    "mq_abi_version": (CINT, []),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+def load_library(path=LIB_PATH):
+    """Load the shared library (no device needed) and bind every symbol."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing: build it with `python -m paper_2506_06258_b200._build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.mq_abi_version() != ABI_VERSION:
+            raise NativeUnavailable("libmarket_eq_b200.so ABI version mismatch")
+        _lib = lib
+        return lib
+
+
+def lib():
+    """The library, after checking that a CUDA device is present."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device: the B200 solver has no CPU fallback")
+    return load_library()
+
+
+def check(rc, what):
+    if rc < 0:
+        msg = load_library().mq_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed ({rc}): {msg}")
+    return rc
+
+
+def ptr(t):
+    """Raw device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else ctypes.c_void_p(t.data_ptr())

@@ -1,0 +1,284 @@
+// Device reductions between chunks: KKT residual ingredients (kkt.py:29-87),
+// the omega_0 residual norms (driver.py:123-132), restart moves
+// (driver.py:156-162) and the Arrow-Debreu budget map E p (exchange.py:89).
+//
+// Determinism: maxima of nonnegative values go through order-free integer
+// atomics on their bit patterns; sums use one partial per block over a grid
+// whose size depends only on the problem size, then a fixed-order final pass.
+#include "mq_common.cuh"
+
+namespace mq {
+
+int sm_count_reduce() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// scratch layout (doubles)
+constexpr int kSlotObj = 0;          // [0, MAXB)      objective partials
+constexpr int kSlotBad = 1;          // [MAXB, 2MAXB)  bad-row counts
+constexpr int kMisc = 8 * MQ_MAX_BLOCKS;  // 64 misc words
+// misc words: [0..3] row maxima bits, [4] first bad row (int64), [8..11] col maxima bits
+
+__global__ void sum_slots_kernel(const double *__restrict__ partials, int nblocks, int nslots,
+                                 double *__restrict__ out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int s = warp; s < nslots; s += blockDim.x >> 5) {
+        double acc = 0.0;
+        for (int b = lane; b < nblocks; b += 32) acc += partials[s * MQ_MAX_BLOCKS + b];
+        acc = group_sum<32>(acc);
+        if (lane == 0) out[s] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+resid_rows_kernel(const mq_market mk, const double *__restrict__ x, const double *__restrict__ p,
+                  int use_norm, double *__restrict__ colbest, double *__restrict__ t_out,
+                  double *__restrict__ y_out, double *__restrict__ scratch) {
+    const double *__restrict__ U = use_norm ? mk.u : mk.u_orig;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double *misc = scratch + kMisc;
+    double ymax = 0.0, gmax = 0.0, xmax = 0.0, emax = 0.0, obj = 0.0, nbad = 0.0;
+    for (int64_t i = warp_id; i < mk.n; i += nwarps) {
+        const int64_t a = mk.row_ptr[i], b = mk.row_ptr[i + 1];
+        double tp = 0.0;
+        for (int64_t t = a + lane; t < b; t += 32) tp += U[t] * x[t];
+        const double t_i = group_sum<32>(tp);
+        if (!(t_i > 0.0)) {
+            if (lane == 0) {
+                nbad += 1.0;
+                atomicMin((unsigned long long *)(misc + 4), (unsigned long long)(mk.row_begin + i));
+                if (t_out) t_out[i] = t_i;
+                if (y_out) y_out[i] = 0.0;
+            }
+            continue;
+        }
+        const double y = mk.w[i] / t_i;
+        if (lane == 0) {
+            obj += mk.w[i] * log(t_i);
+            ymax = fmax(ymax, y);
+            if (t_out) t_out[i] = t_i;
+            if (y_out) y_out[i] = y;
+        }
+        for (int64_t t = a + lane; t < b; t += 32) {
+            const int32_t j = mk.col[t];
+            const double uy = U[t] * y;
+            atomic_max_nonneg(colbest + j, uy);
+            const double es = fmax(p[j] - uy, 0.0);
+            const double xv = x[t];
+            gmax = fmax(gmax, xv * es);
+            xmax = fmax(xmax, fabs(xv));
+            emax = fmax(emax, es);
+        }
+    }
+    gmax = group_max<32>(gmax);
+    xmax = group_max<32>(xmax);
+    emax = group_max<32>(emax);
+    if (lane == 0) {
+        atomic_max_nonneg(misc + 0, ymax);
+        atomic_max_nonneg(misc + 1, gmax);
+        atomic_max_nonneg(misc + 2, xmax);
+        atomic_max_nonneg(misc + 3, emax);
+    }
+    __shared__ double sm[32];
+    const double ob = block_sum(obj, sm);
+    const double nb = block_sum(nbad, sm);
+    if (threadIdx.x == 0) {
+        scratch[kSlotObj * MQ_MAX_BLOCKS + blockIdx.x] = ob;
+        scratch[kSlotBad * MQ_MAX_BLOCKS + blockIdx.x] = nb;
+    }
+}
+
+__global__ void resid_rows_finish(const double *__restrict__ scratch, const double *__restrict__ sums,
+                                  double *__restrict__ row_out) {
+    const double *misc = scratch + kMisc;
+    row_out[0] = misc[0];
+    row_out[1] = misc[1];
+    row_out[2] = misc[2];
+    row_out[3] = misc[3];
+    const unsigned long long bad = __double_as_longlong(misc[4]);
+    row_out[4] = bad == 0xffffffffffffffffull ? -1.0 : (double)(long long)bad;
+    row_out[5] = sums[0];
+    row_out[6] = sums[1];
+    row_out[7] = 0.0;
+}
+
+__global__ void __launch_bounds__(256)
+resid_cols_kernel(int64_t m, const double *__restrict__ cs, const double *__restrict__ p,
+                  const double *__restrict__ colbest, double *__restrict__ scratch) {
+    double *misc = scratch + kMisc;
+    double gap = 0.0, csmax = 0.0, dualp = 0.0, slmax = 0.0, sq1 = 0.0, sq2 = 0.0;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const double c = cs[j];
+        const double sl = p[j] - colbest[j];
+        gap = fmax(gap, fabs(c - 1.0));
+        csmax = fmax(csmax, fabs(c));
+        dualp = fmax(dualp, fmax(-sl, 0.0));
+        slmax = fmax(slmax, sl);
+        sq1 += (c - 1.0) * (c - 1.0);
+        const double d = fmin(sl, 0.0);
+        sq2 += d * d;
+    }
+    gap = group_max<32>(gap);
+    csmax = group_max<32>(csmax);
+    dualp = group_max<32>(dualp);
+    slmax = group_max<32>(slmax);
+    if ((threadIdx.x & 31) == 0) {
+        atomic_max_nonneg(misc + 8, gap);
+        atomic_max_nonneg(misc + 9, csmax);
+        atomic_max_nonneg(misc + 10, dualp);
+        atomic_max_nonneg(misc + 11, slmax);
+    }
+    __shared__ double sm[32];
+    const double a = block_sum(sq1, sm);
+    const double b = block_sum(sq2, sm);
+    if (threadIdx.x == 0) {
+        scratch[2 * MQ_MAX_BLOCKS + blockIdx.x] = a;
+        scratch[3 * MQ_MAX_BLOCKS + blockIdx.x] = b;
+    }
+}
+
+__global__ void resid_cols_finish(const double *__restrict__ scratch, const double *__restrict__ sums,
+                                  double *__restrict__ col_out) {
+    const double *misc = scratch + kMisc;
+    col_out[0] = misc[8];
+    col_out[1] = misc[9];
+    col_out[2] = misc[10];
+    col_out[3] = misc[11];
+    col_out[4] = sums[0];
+    col_out[5] = sums[1];
+}
+
+__global__ void __launch_bounds__(256)
+moves_nnz_kernel(int64_t nnz, const double *__restrict__ xbar, const double *__restrict__ x0,
+                 double *__restrict__ scratch) {
+    double acc = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const double d = xbar[k] - x0[k];
+        acc += d * d;
+    }
+    __shared__ double sm[32];
+    const double r = block_sum(acc, sm);
+    if (threadIdx.x == 0) scratch[blockIdx.x] = r;
+}
+
+__global__ void __launch_bounds__(256)
+moves_m_kernel(int64_t m, const double *__restrict__ pbar, const double *__restrict__ p0,
+               const double *__restrict__ csbar, const double *__restrict__ cs0,
+               double *__restrict__ scratch) {
+    double a = 0.0, b = 0.0;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const double dp = pbar[j] - p0[j];
+        a += dp * dp;
+        b += (csbar[j] - cs0[j]) * dp;
+    }
+    __shared__ double sm[32];
+    const double ra = block_sum(a, sm);
+    const double rb = block_sum(b, sm);
+    if (threadIdx.x == 0) {
+        scratch[MQ_MAX_BLOCKS + blockIdx.x] = ra;
+        scratch[2 * MQ_MAX_BLOCKS + blockIdx.x] = rb;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+spmv_kernel(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+            const double *__restrict__ val, const double *__restrict__ v, double *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp_id; i < n; i += nwarps) {
+        double acc = 0.0;
+        for (int64_t t = row_ptr[i] + lane; t < row_ptr[i + 1]; t += 32) acc += val[t] * v[col[t]];
+        acc = group_sum<32>(acc);
+        if (lane == 0) out[i] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+normalize_kernel(int64_t n, const int64_t *__restrict__ row_ptr, const double *__restrict__ u,
+                 double *__restrict__ u_out, double *__restrict__ scales) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp_id; i < n; i += nwarps) {
+        const int64_t a = row_ptr[i], b = row_ptr[i + 1];
+        double mx = 0.0;
+        for (int64_t t = a + lane; t < b; t += 32) mx = fmax(mx, u[t]);
+        mx = group_max<32>(mx);
+        for (int64_t t = a + lane; t < b; t += 32) u_out[t] = u[t] / mx;
+        if (lane == 0) scales[i] = mx;
+    }
+}
+
+}  // namespace mq
+
+using namespace mq;
+
+extern "C" {
+
+int64_t mq_scratch_doubles(void) { return MQ_SCRATCH_DOUBLES; }
+
+int mq_resid_rows(const mq_market *mk, const double *x, const double *p, int use_norm,
+                  double *colbest, double *t_out, double *y_out, double *row_out, double *scratch,
+                  void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int grid = grid_for(mk->n, 8, MQ_MAX_BLOCKS);
+    cudaMemsetAsync(scratch + kMisc, 0, 4 * sizeof(double), s);
+    cudaMemsetAsync(scratch + kMisc + 4, 0xff, sizeof(double), s);
+    resid_rows_kernel<<<grid, 256, 0, s>>>(*mk, x, p, use_norm, colbest, t_out, y_out, scratch);
+    sum_slots_kernel<<<1, 64, 0, s>>>(scratch, grid, 2, scratch + kMisc + 16);
+    resid_rows_finish<<<1, 1, 0, s>>>(scratch, scratch + kMisc + 16, row_out);
+    return check_launch("mq_resid_rows");
+}
+
+int mq_resid_cols(int64_t m, const double *cs, const double *p, const double *colbest,
+                  double *col_out, double *scratch, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int grid = grid_for(m, 256, MQ_MAX_BLOCKS);
+    cudaMemsetAsync(scratch + kMisc + 8, 0, 4 * sizeof(double), s);
+    resid_cols_kernel<<<grid, 256, 0, s>>>(m, cs, p, colbest, scratch);
+    sum_slots_kernel<<<1, 64, 0, s>>>(scratch + 2 * MQ_MAX_BLOCKS, grid, 2, scratch + kMisc + 20);
+    resid_cols_finish<<<1, 1, 0, s>>>(scratch, scratch + kMisc + 20, col_out);
+    return check_launch("mq_resid_cols");
+}
+
+int mq_restart_moves(const mq_market *mk, const double *xbar, const double *x0, const double *pbar,
+                     const double *p0, const double *csbar, const double *cs0, double *out,
+                     double *scratch, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int g1 = grid_for(mk->nnz, 2048, MQ_MAX_BLOCKS);
+    const int g2 = grid_for(mk->m, 256, MQ_MAX_BLOCKS);
+    moves_nnz_kernel<<<g1, 256, 0, s>>>(mk->nnz, xbar, x0, scratch);
+    moves_m_kernel<<<g2, 256, 0, s>>>(mk->m, pbar, p0, csbar, cs0, scratch);
+    sum_slots_kernel<<<1, 32, 0, s>>>(scratch, g1, 1, out);
+    sum_slots_kernel<<<1, 64, 0, s>>>(scratch + MQ_MAX_BLOCKS, g2, 2, out + 1);
+    return check_launch("mq_restart_moves");
+}
+
+int mq_normalize_rows(int64_t n, const int64_t *row_ptr, const double *u, double *u_out,
+                      double *scales, void *stream) {
+    const int grid = grid_for(n, 8, sm_count_reduce() * 16);
+    normalize_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(n, row_ptr, u, u_out, scales);
+    return check_launch("mq_normalize_rows");
+}
+
+int mq_spmv(int64_t n_rows, const int64_t *row_ptr, const int32_t *col, const double *val,
+            const double *v, double *out, void *stream) {
+    const int grid = grid_for(n_rows, 8, sm_count_reduce() * 16);
+    spmv_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(n_rows, row_ptr, col, val, v, out);
+    return check_launch("mq_spmv");
+}
+
+}  // extern "C"

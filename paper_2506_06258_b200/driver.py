@@ -1,0 +1,208 @@
+"""Restarted PDHCG solve on the B200 (market_eq/driver.py:35-377, PDHCG branch).
+
+The control flow is the reference's, decision for decision: validate,
+normalize, initial (or warm) state, operator norm L, omega_0 from the
+residual norms, StepController(eta 0.9/L, cap 0.95/L, omega band x16),
+chunks of `check_every` iterations, residuals of the last and the averaged
+iterate on the original instance, metric = min of the two, stop at tol or the
+iteration cap (adopting the better iterate), adaptive restart test, restart
+moves -> controller update -> restart to the average.
+
+What moved to the device: every nnz- or m-sized operation (the chunk, the
+column sums, residuals, omega_0 norms, restart moves, normalization, the
+transpose schedule).  The host keeps only scalars.
+"""
+
+import logging
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from .adaptive import RestartParams, StepController, should_restart, update_weights
+from .errors import ValidationError
+from .instance import validate
+from .report import SolveReport, instance_fingerprint
+from .sparse import selector_norm_from_counts
+
+log = logging.getLogger("market_eq")
+
+OMEGA_BOUND_FACTOR = 16.0  # driver.py:31
+
+
+@dataclass
+class SolveConfig:
+    tol: float = 1e-4
+    max_iters: int = 100_000
+    restart: str = "adaptive"          # "adaptive" or "fixed"
+    restart_k: int = 0                 # inner length when restart == "fixed"
+    sections: int = 32                 # k-section grid (row_solver="ksection")
+    subproblem_tol: float = 1e-10      # k-section bracket width (row_solver="ksection")
+    step_mode: str = "adaptive"        # "theory" or "adaptive"
+    adapt_eta: bool = True
+    check_every: int = 40
+    threads: int = None                # accepted for API compatibility (no CPU threads)
+    restart_params: RestartParams = field(default_factory=RestartParams)
+    # B200 additions
+    row_solver: str = "exact"          # "exact" (active-set closed form) or "ksection"
+    device: object = None              # torch device / index; default current CUDA device
+    use_graphs: bool = True            # CUDA-graph capture of chunks
+
+    def __post_init__(self):
+        if self.tol <= 0:
+            raise ValueError("tol must be positive")
+        if self.restart not in ("adaptive", "fixed"):
+            raise ValueError("restart must be 'adaptive' or 'fixed'")
+        if self.restart == "fixed" and self.restart_k < 1:
+            raise ValueError("fixed restart needs restart_k >= 1")
+        if self.step_mode not in ("theory", "adaptive"):
+            raise ValueError("step_mode must be 'theory' or 'adaptive'")
+        if self.sections < 2:
+            raise ValueError("sections must be >= 2")
+        if self.check_every < 1:
+            raise ValueError("check_every must be >= 1")
+        if self.row_solver not in ("exact", "ksection"):
+            raise ValueError("row_solver must be 'exact' or 'ksection'")
+
+    def with_overrides(self, **kw):
+        return replace(self, **kw)
+
+    def as_dict(self):
+        rp = self.restart_params
+        return {
+            "tol": self.tol, "max_iters": self.max_iters,
+            "restart": f"fixed:{self.restart_k}" if self.restart == "fixed" else "adaptive",
+            "sections": self.sections, "subproblem_tol": self.subproblem_tol,
+            "step_mode": self.step_mode, "adapt_eta": self.adapt_eta,
+            "check_every": self.check_every, "threads": self.threads,
+            "beta_sufficient": rp.beta_sufficient, "beta_necessary": rp.beta_necessary,
+            "beta_artificial": rp.beta_artificial, "row_solver": self.row_solver,
+        }
+
+
+class DeviceSession:
+    """Device market + engine kept alive across solves of the same utilities
+    (Arrow-Debreu re-solves with new budgets; benchmarks)."""
+
+    def __init__(self, inst, cfg, group=None, dm=None):
+        from .device import DeviceMarket
+        from .engine import PdhcgEngine
+
+        self.dm = dm if dm is not None else DeviceMarket.from_instance(inst, device=cfg.device)
+        self.engine = PdhcgEngine(self.dm, row_solver=cfg.row_solver, sections=cfg.sections,
+                                  subproblem_tol=cfg.subproblem_tol, use_graphs=cfg.use_graphs,
+                                  group=group)
+        counts = self.engine._global_counts().cpu().numpy()
+        self.op_norm = selector_norm_from_counts(counts)
+
+
+def solve_on_device(session, cfg, warm_start=None, w_sum=None, inst=None, algo="pdhcg"):
+    """The restarted loop of driver.py:271-377 against a DeviceSession."""
+    eng = session.engine
+    if warm_start is not None:
+        x = np.asarray(warm_start["x"], dtype=np.float64)
+        p = np.asarray(warm_start["p"], dtype=np.float64)
+        if x.shape != (session.dm.nnz,) or p.shape != (session.dm.m,):
+            raise ValueError("warm start shapes do not match the instance")
+        eng.load_state(x, p)
+    else:
+        eng.initial_state(w_sum=w_sum)
+
+    L = max(session.op_norm, np.finfo(float).tiny)
+    if cfg.step_mode == "theory":
+        controller = None
+        tau = sigma = 1.0 / (2.0 * L)
+        if warm_start is not None:
+            eng.omega_norms()  # zero-utility check of the warm start
+    else:
+        primal_res, dual_res = eng.omega_norms()
+        if primal_res > 1e-8 and dual_res > 1e-8:
+            omega0 = max(1.0, dual_res / primal_res)
+        else:
+            omega0 = 1.0
+        controller = StepController(eta_initial=0.9 / L, omega_initial=omega0, eta_max=0.95 / L,
+                                    omega_lower=omega0 / OMEGA_BOUND_FACTOR,
+                                    omega_upper=omega0 * OMEGA_BOUND_FACTOR)
+        tau, sigma = controller.tau, controller.sigma
+    eng.set_steps(tau, sigma)
+    log.info("%s solve on %s: n=%d m=%d nnz=%d L=%.3g tau=%.3g sigma=%.3g", algo,
+             session.dm.device, session.dm.n, session.dm.m, session.dm.nnz, L, tau, sigma)
+
+    res_avg = eng.residuals_avg()
+    metric_last_restart = metric_prev_check = res_avg.rel_kkt
+    history, passes = [], []
+    total = restarts = 0
+    chunk_time = 0.0
+    t0 = time.perf_counter()
+    while True:
+        chunk = min(cfg.check_every, cfg.max_iters - total)
+        if cfg.restart == "fixed":
+            chunk = min(chunk, cfg.restart_k - eng.navg)
+        tc = time.perf_counter()
+        passes.extend(eng.run_chunk(chunk))
+        chunk_time += time.perf_counter() - tc
+        total += chunk
+        res_last, res_avg = eng.residuals_pair()
+        metric = min(res_last.rel_kkt, res_avg.rel_kkt)
+        history.append((total, metric))
+        if metric <= cfg.tol or total >= cfg.max_iters:
+            if res_avg.rel_kkt < res_last.rel_kkt:
+                eng.adopt_average()
+                final = res_avg
+            else:
+                final = res_last
+            status = "optimal" if metric <= cfg.tol else "max-iters"
+            break
+        if cfg.restart == "fixed":
+            do_restart = eng.navg >= cfg.restart_k
+        else:
+            do_restart = should_restart(res_avg.rel_kkt, metric_last_restart, metric_prev_check,
+                                        eng.navg, total, cfg.restart_params)
+        metric_prev_check = res_avg.rel_kkt
+        if do_restart:
+            if controller is not None:
+                pm, dm_, psq, dsq, inter = eng.restart_moves()
+                eta_obs = None
+                if cfg.adapt_eta and inter > 0.0:
+                    eta_obs = (controller.omega * psq + dsq / controller.omega) / (2.0 * inter)
+                update_weights(controller, pm, dm_, eta_obs)
+                eng.set_steps(controller.tau, controller.sigma)
+            eng.restart()
+            restarts += 1
+            eng.snapshot()
+            metric_last_restart = metric_prev_check = res_avg.rel_kkt
+    wall = time.perf_counter() - t0
+    log.info("%s finished: status=%s iters=%d restarts=%d rel_kkt=%.3g (%.2fs)", algo, status,
+             total, restarts, final.rel_kkt, wall)
+    payload = eng.final_payload()
+    echo = cfg.as_dict()
+    echo["algo"] = algo
+    objective = payload.pop("objective")
+    return SolveReport(
+        solver=algo, status=status, inner_iterations=total, restarts=restarts,
+        wall_time_seconds=wall, final_residuals=final, residual_history=history,
+        instance_fingerprint=instance_fingerprint(inst) if inst is not None else "",
+        config_echo=echo, subproblem_passes=passes, objective=objective,
+        device_stats={"chunk_seconds": chunk_time,
+                      "iters_per_second": total / chunk_time if chunk_time > 0 else None,
+                      "op_norm": L, "device": str(session.dm.device)},
+        **payload)
+
+
+def run_solve(inst, cfg, algo, warm_start=None):
+    """Restarted solve of a Fisher instance on the GPU; returns a SolveReport.
+
+    `warm_start`, when given, is a dict {"x": entry-aligned allocation,
+    "p": prices}.  Only algo="pdhcg" is provided (lifted PDHG is out of scope
+    for this hot path).
+    """
+    violations = validate(inst)
+    if violations:
+        raise ValidationError("; ".join(violations))
+    if algo != "pdhcg":
+        if algo == "pdhg":
+            raise NotImplementedError("lifted PDHG is not part of the B200 hot path yet")
+        raise ValueError(f"unknown algorithm {algo!r}")
+    session = DeviceSession(inst, cfg)
+    return solve_on_device(session, cfg, warm_start=warm_start,
+                           w_sum=float(np.sum(inst.budgets)), inst=inst)

@@ -1,0 +1,348 @@
+"""PDHCG iterate on the device: chunks, residuals, restarts.
+
+`PdhcgEngine` owns the iterate of driver._CompactRun (driver.py:91-181) as
+torch buffers and runs everything through the native library:
+
+* row_solver="exact" (default): one iteration = mq_dual_step +
+  mq_primal_step + mq_colsum_step, all scalars device-resident, a chunk of
+  `iters` iterations captured once per length as a CUDA graph and replayed;
+  on N GPUs the column sums are all-reduced between colsum and the next price
+  step (NCCL over NVLink), everything else stays rank-local.
+* row_solver="ksection": the bit-faithful drop-in mq_pdhcg_chunk (literal
+  k-section search, serial reference sums), single GPU.
+
+Residuals (kkt.py:29-87), the omega_0 norms (driver.py:123-132) and restart
+moves (driver.py:156-162) are device reductions that hand back a handful of
+scalars per check.
+"""
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .errors import SubproblemError
+from .kkt import Residuals
+
+MAX_ROW_PASSES = 200  # kernels.py:16 (k-section fault threshold)
+
+
+def _cur_stream():
+    import ctypes
+
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class PdhcgEngine:
+    def __init__(self, dm, row_solver="exact", sections=32, subproblem_tol=1e-10,
+                 use_graphs=True, group=None):
+        if row_solver not in ("exact", "ksection"):
+            raise ValueError("row_solver must be 'exact' or 'ksection'")
+        self.dm = dm
+        self.lib = dm.lib
+        self.mode = row_solver
+        self.sections = int(sections)
+        self.subtol = float(subproblem_tol)
+        self.group = group
+        self.world = 1
+        if group is not None:
+            import torch.distributed as dist
+
+            self.world = dist.get_world_size(group)
+        if self.mode == "ksection" and self.world > 1:
+            raise ValueError("the k-section drop-in runs on a single GPU")
+        self.use_graphs = bool(use_graphs) and self.world == 1
+        dev = dm.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        nnz, m = dm.nnz, dm.m
+        self.x = torch.zeros(nnz, **f64)
+        self.xbar = torch.zeros(nnz, **f64)
+        self.x0 = torch.zeros(nnz, **f64)
+        self.p = torch.zeros(m, **f64)
+        self.pbar = torch.zeros(m, **f64)
+        self.p0 = torch.zeros(m, **f64)
+        self.cs = torch.zeros(m, **f64)
+        self.cs_prev = torch.zeros(m, **f64)
+        self.csbar = torch.zeros(m, **f64)
+        self.cs0 = torch.zeros(m, **f64)
+        self.colbest = torch.zeros(2, m, **f64)
+        self.steps = torch.zeros(2, **f64)
+        self.navg_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.faults = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.pass_buf = torch.zeros(1024, dtype=torch.int64, device=dev)
+        self.scratch = torch.zeros(int(self.lib.mq_scratch_doubles()), **f64)
+        self.scratch2 = torch.zeros(int(self.lib.mq_scratch_doubles()), **f64)
+        self.out = torch.zeros(32, **f64)
+        self.t_buf = torch.zeros(dm.n, **f64)
+        if self.mode == "ksection":
+            self.x_prev = torch.zeros(nnz, **f64)
+            self.c_buf = torch.zeros(nnz, **f64)
+        self.navg = 0
+        self.tau = self.sigma = None
+        self._graphs = {}
+        self.state = self._make_state()
+
+    # ------------------------------------------------------------ plumbing
+    def _make_state(self):
+        s = nat.MqState()
+        for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "steps", "faults"):
+            setattr(s, name, getattr(self, name).data_ptr())
+        s.navg = self.navg_dev.data_ptr()
+        s.pass_out = self.pass_buf.data_ptr()
+        return s
+
+    def _allreduce(self, t, op="sum"):
+        if self.world > 1:
+            import torch.distributed as dist
+
+            red = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX,
+                   "min": dist.ReduceOp.MIN}[op]
+            dist.all_reduce(t, op=red, group=self.group)
+        return t
+
+    def colsum(self, v, out):
+        nat.check(self.lib.mq_colsum(self.dm.struct, nat.ptr(v), nat.ptr(out), _cur_stream()),
+                  "mq_colsum")
+        return self._allreduce(out)
+
+    # ------------------------------------------------------------ state
+    def load_state(self, x, p):
+        """Start (or warm start) from allocation x and prices p."""
+        self.x.copy_(torch.as_tensor(x, dtype=torch.float64))
+        self.p.copy_(torch.as_tensor(p, dtype=torch.float64))
+        self.xbar.copy_(self.x)
+        self.pbar.copy_(self.p)
+        if self.mode == "ksection":
+            self.x_prev.copy_(self.x)
+        self.colsum(self.x, self.cs)
+        self.cs_prev.copy_(self.cs)
+        self.csbar.copy_(self.cs)
+        self.navg = 0
+        self.navg_dev.zero_()
+        self.snapshot()
+
+    def load_full_state(self, x, x_prev, p, xbar, pbar, navg):
+        """Mid-run state of kernels.pdhcg_chunk's argument list (lockstep tests)."""
+        f = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.float64)  # noqa: E731
+        self.x.copy_(f(x))
+        self.p.copy_(f(p))
+        self.xbar.copy_(f(xbar))
+        self.pbar.copy_(f(pbar))
+        self.colsum(self.x, self.cs)
+        self.colsum(self.xbar, self.csbar)
+        if self.mode == "ksection":
+            self.x_prev.copy_(f(x_prev))
+            self.colsum(self.x_prev, self.cs_prev)
+        else:
+            xp = torch.as_tensor(np.asarray(x_prev), dtype=torch.float64, device=self.x.device)
+            self.colsum(xp, self.cs_prev)
+        self.navg = int(navg)
+        self.navg_dev.fill_(self.navg)
+        self.snapshot()
+
+    def initial_state(self, w_sum=None):
+        """x_ij = 1/colcount_j, p_j = sum(w)/m (pdhcg.py:66-72)."""
+        counts = self._global_counts()
+        x = 1.0 / counts.to(torch.float64)[self.dm.col.to(torch.int64)]
+        if w_sum is None:
+            w_sum = float(self._allreduce(self.dm.w.sum().reshape(1)).item())
+        p = torch.full((self.dm.m,), w_sum / self.dm.m, dtype=torch.float64,
+                       device=self.dm.device)
+        self.load_state(x, p)
+
+    def _global_counts(self):
+        return self._allreduce(self.dm.col_counts.clone())
+
+    def set_steps(self, tau, sigma):
+        if (tau, sigma) != (self.tau, self.sigma):
+            self.tau, self.sigma = float(tau), float(sigma)
+            self.steps.copy_(torch.tensor([self.tau, self.sigma], dtype=torch.float64))
+
+    def snapshot(self):
+        self.x0.copy_(self.x)
+        self.p0.copy_(self.p)
+        self.cs0.copy_(self.cs)
+
+    def restart(self):
+        """x <- xbar, p <- pbar, x_prev <- x, navg <- 0 (driver.py:164-168)."""
+        self.x.copy_(self.xbar)
+        self.p.copy_(self.pbar)
+        self.cs.copy_(self.csbar)
+        self.cs_prev.copy_(self.csbar)
+        if self.mode == "ksection":
+            self.x_prev.copy_(self.x)
+        self.navg = 0
+        self.navg_dev.zero_()
+
+    def adopt_average(self):
+        self.x.copy_(self.xbar)
+        self.p.copy_(self.pbar)
+        self.cs.copy_(self.csbar)
+
+    # ------------------------------------------------------------ chunks
+    def run_chunk(self, iters):
+        """`iters` PDHCG iterations; returns the per-iteration work counts.
+        Raises SubproblemError on faulted rows (driver.py:142-144)."""
+        if self.mode == "ksection":
+            return self._run_chunk_ksection(iters)
+        if iters > self.pass_buf.numel():
+            raise ValueError("chunk longer than the pass buffer")
+        if self.use_graphs:
+            g = self._graphs.get(iters)
+            if g is None:
+                g = self._capture(iters)
+            g.replay()
+        else:
+            self._launch_chunk(iters)
+        self.navg += iters
+        vals = torch.cat([self.pass_buf[:iters], self.faults]).cpu().numpy()
+        if vals[-1]:
+            raise SubproblemError(f"{int(vals[-1])} row subproblems failed to converge")
+        return [int(v) for v in vals[:-1]]
+
+    def _launch_chunk(self, iters):
+        lib, mk, st = self.lib, self.dm.struct, self.state
+        self.pass_buf[:iters].zero_()
+        self.faults.zero_()
+        fin = 1 if self.world == 1 else 0
+        for it in range(iters):
+            s = _cur_stream()
+            nat.check(lib.mq_dual_step(mk, st, it, s), "mq_dual_step")
+            nat.check(lib.mq_primal_step(mk, st, it, None, s), "mq_primal_step")
+            nat.check(lib.mq_colsum_step(mk, st, it, fin, s), "mq_colsum_step")
+            if not fin:
+                self._allreduce(self.cs)
+                nat.check(lib.mq_colsum_finalize(mk, st, it, s), "mq_colsum_finalize")
+        if self.world > 1:
+            self._allreduce(self.pass_buf[:iters])
+            self._allreduce(self.faults)
+        nat.check(lib.mq_chunk_end(st, iters, _cur_stream()), "mq_chunk_end")
+
+    def _capture(self, iters):
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=self.dm.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            torch.cuda.synchronize(self.dm.device)
+        with torch.cuda.graph(g, stream=side):
+            self._launch_chunk(iters)
+        torch.cuda.current_stream().wait_stream(side)
+        self._graphs[iters] = g
+        return g
+
+    def _run_chunk_ksection(self, iters):
+        import ctypes
+
+        dm = self.dm
+        navg_out = ctypes.c_int64(0)
+        self.set_steps(self.tau, self.sigma)
+        rc = self.lib.mq_pdhcg_chunk(
+            dm.n, dm.m, nat.ptr(dm.row_ptr), nat.ptr(dm.col), nat.ptr(dm.u), nat.ptr(dm.tperm),
+            nat.ptr(dm.tptr), nat.ptr(dm.w), nat.ptr(self.x), nat.ptr(self.x_prev),
+            nat.ptr(self.p), nat.ptr(self.xbar), nat.ptr(self.pbar), self.navg, self.tau,
+            self.sigma, self.sections, self.subtol, iters, nat.ptr(self.c_buf),
+            nat.ptr(self.pass_buf), ctypes.byref(navg_out), _cur_stream())
+        nat.check(rc, "mq_pdhcg_chunk")
+        if rc > 0:
+            raise SubproblemError(f"{rc} row subproblems exceeded {MAX_ROW_PASSES} passes")
+        self.navg = int(navg_out.value)
+        self.navg_dev.fill_(self.navg)
+        # column sums of the iterates for residuals / restart moves
+        self.colsum(self.x, self.cs)
+        self.colsum(self.x_prev, self.cs_prev)
+        self.colsum(self.xbar, self.csbar)
+        return [int(v) for v in self.pass_buf[:iters].cpu().numpy()]
+
+    # ------------------------------------------------------------ reductions
+    def _rows(self, x, p, use_norm, k, t_out=None):
+        self.colbest[k].zero_()
+        nat.check(self.lib.mq_resid_rows(self.dm.struct, nat.ptr(x), nat.ptr(p), int(use_norm),
+                                         nat.ptr(self.colbest[k]), nat.ptr(t_out), None,
+                                         nat.ptr(self.out[16 * k: 16 * k + 8]),
+                                         nat.ptr(self.scratch if k == 0 else self.scratch2),
+                                         _cur_stream()), "mq_resid_rows")
+        if self.world > 1:
+            o = self.out[16 * k: 16 * k + 8]
+            self._allreduce(self.colbest[k], "max")
+            mx = o[0:4].clone()
+            self._allreduce(mx, "max")
+            o[0:4].copy_(mx)
+            bad = torch.where(o[4:5] < 0, torch.full_like(o[4:5], math.inf), o[4:5])
+            self._allreduce(bad, "min")
+            o[4:5].copy_(torch.where(torch.isinf(bad), torch.full_like(bad, -1.0), bad))
+            sm = o[5:7].clone()
+            self._allreduce(sm, "sum")
+            o[5:7].copy_(sm)
+
+    def _cols(self, cs, p, k):
+        nat.check(self.lib.mq_resid_cols(self.dm.m, nat.ptr(cs), nat.ptr(p),
+                                         nat.ptr(self.colbest[k]),
+                                         nat.ptr(self.out[16 * k + 8: 16 * k + 14]),
+                                         nat.ptr(self.scratch if k == 0 else self.scratch2),
+                                         _cur_stream()), "mq_resid_cols")
+
+    @staticmethod
+    def _assemble(v):
+        ymax, gmax, xmax, emax, bad, _obj, nbad = v[0:7]
+        colgap, csmax, dualp, slmax = v[8:12]
+        if nbad > 0:
+            raise ValueError(f"buyer {int(bad)} has zero utility value; state is not a "
+                             "valid compact iterate")
+        r_primal = colgap / (1.0 + max(csmax, 0.0, 1.0))
+        r_dual = max(0.0, dualp) / (1.0 + max(ymax, ymax, slmax))
+        r_gap = gmax / (1.0 + max(xmax, emax))
+        return Residuals(float(r_primal), float(r_dual), float(r_gap),
+                         float(max(r_primal, r_dual, r_gap)))
+
+    def residuals_pair(self):
+        """(last, avg) residuals on the ORIGINAL instance with one sync."""
+        self._rows(self.x, self.p, 0, 0)
+        self._cols(self.cs, self.p, 0)
+        self._rows(self.xbar, self.pbar, 0, 1)
+        self._cols(self.csbar, self.pbar, 1)
+        v = self.out.cpu().numpy()
+        return self._assemble(v[0:16]), self._assemble(v[16:32])
+
+    def residuals_avg(self):
+        self._rows(self.xbar, self.pbar, 0, 1)
+        self._cols(self.csbar, self.pbar, 1)
+        return self._assemble(self.out[16:32].cpu().numpy())
+
+    def omega_norms(self):
+        """(||colsum(x)-1||_2, ||min(p - max_col u y, 0)||_2) on the normalized
+        instance (driver.py:123-132)."""
+        self._rows(self.x, self.p, 1, 0)
+        self._cols(self.cs, self.p, 0)
+        v = self.out[0:16].cpu().numpy()
+        if v[6] > 0:
+            raise ValueError("warm start gives some buyer zero utility")
+        return math.sqrt(v[12]), math.sqrt(v[13])
+
+    def restart_moves(self):
+        """(||dx||, ||dp||, ||dx||^2, ||dp||^2, |colsum(dx).dp|) of the average
+        against the last restart point (driver.py:156-162)."""
+        o = self.out[24:28]
+        nat.check(self.lib.mq_restart_moves(self.dm.struct, nat.ptr(self.xbar), nat.ptr(self.x0),
+                                            nat.ptr(self.pbar), nat.ptr(self.p0),
+                                            nat.ptr(self.csbar), nat.ptr(self.cs0), nat.ptr(o),
+                                            nat.ptr(self.scratch), _cur_stream()),
+                  "mq_restart_moves")
+        if self.world > 1:
+            sx = o[0:1].clone()
+            self._allreduce(sx, "sum")
+            o[0:1].copy_(sx)
+        dxx, dpp, inter = (float(v) for v in o[0:3].cpu().numpy())
+        return math.sqrt(dxx), math.sqrt(dpp), dxx, dpp, abs(inter)
+
+    def final_payload(self):
+        """prices, allocation, utility values, dual values, objective."""
+        self._rows(self.x, self.p, 0, 0, t_out=self.t_buf)
+        v = self.out[0:8].cpu().numpy()
+        t = self.t_buf.cpu().numpy()
+        w = self.dm.w.cpu().numpy()
+        with np.errstate(divide="ignore"):
+            y = w / t
+        obj = -float(v[5]) if v[6] == 0 else math.inf
+        return {"prices": self.p.cpu().numpy(), "allocation": self.x.cpu().numpy(),
+                "utility_values": t, "dual_values": y, "objective": obj}

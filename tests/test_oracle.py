@@ -1,0 +1,142 @@
+"""The CPU oracle is pinned to the reference: every golden vector the
+reference produced (oracle/gen_golden.py) must be reproduced bit for bit."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden, golden_names
+from _helpers import instance_from, oracle_market
+
+
+@pytest.mark.parametrize("name", golden_names("chunk_"))
+def test_oracle_chunk_bit_exact(name, oracle):
+    g = golden(name)
+    st = {k: g[f"in_{k}"].copy() for k in ("x", "x_prev", "p", "xbar", "pbar")}
+    passes = np.zeros(int(g["iters"]), dtype=np.int64)
+    navg, faults = oracle.pdhcg_chunk(g["indptr"], g["col"], g["u"], g["tperm"], g["tindptr"],
+                                      g["w"], st["x"], st["x_prev"], st["p"], st["xbar"],
+                                      st["pbar"], int(g["navg_in"]), float(g["tau"]),
+                                      float(g["sigma"]), int(g["sections"]), float(g["subtol"]),
+                                      int(g["iters"]), np.empty(len(g["u"])), passes)
+    for k in st:
+        assert np.array_equal(st[k], g[f"out_{k}"]), k
+    assert np.array_equal(passes, g["passes"])
+    assert navg == int(g["navg_out"]) and faults == int(g["faults"])
+
+
+def test_oracle_chunk_thread_invariant(oracle):
+    g = golden("chunk_powerlaw400.npz")
+    outs = []
+    for threads in (1, 3, 8):
+        oracle.set_threads(threads)
+        st = {k: g[f"in_{k}"].copy() for k in ("x", "x_prev", "p", "xbar", "pbar")}
+        oracle.pdhcg_chunk(g["indptr"], g["col"], g["u"], g["tperm"], g["tindptr"], g["w"],
+                           st["x"], st["x_prev"], st["p"], st["xbar"], st["pbar"],
+                           int(g["navg_in"]), float(g["tau"]), float(g["sigma"]), 32, 1e-10,
+                           int(g["iters"]), np.empty(len(g["u"])),
+                           np.zeros(int(g["iters"]), dtype=np.int64))
+        outs.append(st)
+    oracle.set_threads(os.cpu_count() or 1)
+    for st in outs[1:]:
+        for k in st:
+            assert np.array_equal(st[k], outs[0][k])
+
+
+def test_oracle_row_root_bit_exact(oracle):
+    g = golden("rowroot.npz")
+    ptr = g["ptr"]
+    for r in range(len(ptr) - 1):
+        u = g["u"][ptr[r]:ptr[r + 1]]
+        c = g["c"][ptr[r]:ptr[r + 1]]
+        tw, s0, sec, tol = g["meta"][r]
+        s, npass = oracle.row_root(u, c, tw, s0, int(sec), tol)
+        assert s == g["s"][r] and npass == g["passes"][r], r
+
+
+def test_spec_sqrt2_row(oracle):
+    # u=[1,1], w=1, tau=1, p=[1,1], x^k=[1,1] -> s = sqrt(2)
+    s, _ = oracle.row_root(np.ones(2), np.zeros(2), 1.0, 2.0, 32, 1e-12)
+    assert abs(s - np.sqrt(2.0)) < 1e-11
+
+
+def _oracle_solve_kwargs(g):
+    kw = dict(tol=float(g["tol"]), sections=int(g["sections"]), subtol=float(g["subtol"]))
+    if "restart" in g.files:
+        kw.update(restart=str(g["restart"]), restart_k=int(g["restart_k"]),
+                  step_mode=str(g["step_mode"]), max_iters=int(g["max_iters"]))
+    return kw
+
+
+SMALL = [n for n in golden_names("solve_") if "n" in np.load(os.path.join(GOLDEN, n)).files]
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_oracle_solve_bit_exact(name, oracle):
+    g = golden(name)
+    inst = instance_from(g)
+    o = oracle.solve(oracle_market(inst), **_oracle_solve_kwargs(g))
+    assert o["status"] == str(g["status"])
+    assert o["inner_iterations"] == int(g["iters"]) and o["restarts"] == int(g["restarts"])
+    assert np.array_equal(o["prices"], g["prices"])
+    assert np.array_equal(o["allocation"], g["allocation"])
+    assert np.array_equal(np.asarray(o["residual_history"]), g["history"])
+    assert np.array_equal(np.asarray(o["final_residuals"]), g["final"])
+    assert np.array_equal(np.asarray(o["subproblem_passes"]), g["passes"])
+    assert o["objective"] == float(g["objective"])
+
+
+@pytest.mark.slow
+def test_oracle_solve_spec1000(oracle):
+    import paper_2506_06258_b200 as mq
+
+    g = golden("solve_spec1000.npz")
+    inst = mq.generate_fisher(mq.GeneratorConfig(n=1000, m=400, sparsity_u=0.2, seed=0))
+    o = oracle.solve(oracle_market(inst), **_oracle_solve_kwargs(g))
+    assert o["inner_iterations"] == int(g["iters"])
+    assert np.array_equal(o["prices"], g["prices"])
+
+
+def test_oracle_residuals_bit_exact(oracle):
+    g = golden("resid.npz")
+    mk = oracle_market(instance_from(g))
+    for x, p, r, obj in zip(g["x"], g["p"], g["r"], g["objective"]):
+        assert np.array_equal(np.asarray(oracle.residuals_compact(mk, x, p)), r)
+        assert oracle.eg_objective(mk, x) == obj
+
+
+def test_oracle_exchange_matches_reference(oracle):
+    g = golden("exchange.npz")
+    U = oracle.Market(int(g["n"]), int(g["m"]), g["u_indptr"], g["u_col"], g["u"],
+                      np.ones(int(g["n"])))
+    E = oracle.Market(int(g["n"]), int(g["m"]), g["e_indptr"], g["e_col"], g["e"],
+                      np.ones(int(g["n"])))
+    o = oracle.solve_exchange(U, E, outer_tol=1e-6)
+    assert o["status"] == str(g["status"]) and o["outer_iterations"] == int(g["outer"])
+    assert np.array_equal(o["budget_gaps"], g["gaps"])
+    assert np.array_equal(o["final_prices"], g["final_prices"])
+
+
+def test_generator_fingerprints_match_reference():
+    """The package's host generator reproduces the reference's instances."""
+    import paper_2506_06258_b200 as mq
+
+    fps = json.load(open(os.path.join(GOLDEN, "gen.json")))
+    checked = 0
+    for key, rec in fps.items():
+        parts = key.split(":")
+        if parts[0] == "fisher":
+            n, m, q, seed = int(parts[1]), int(parts[2]), float(parts[3]), int(parts[4])
+            if n * m > 5_000_000:
+                continue
+            inst = mq.generate_fisher(mq.GeneratorConfig(n=n, m=m, sparsity_u=q, seed=seed))
+        else:
+            n, m, q, qe, seed = (int(parts[1]), int(parts[2]), float(parts[3]),
+                                 float(parts[4]), int(parts[5]))
+            inst = mq.generate_exchange(mq.GeneratorConfig(n=n, m=m, sparsity_u=q,
+                                                           sparsity_e=qe, seed=seed))
+        assert mq.instance_fingerprint(inst) == rec["fingerprint"], key
+        checked += 1
+    assert checked >= 6
