@@ -154,6 +154,21 @@ int mq_spmv(int64_t n_rows, const int64_t *row_ptr, const int32_t *col,
 int mq_normalize_rows(int64_t n, const int64_t *row_ptr, const double *u, double *u_out,
                       double *scales, void *stream);
 
+/* ---- device instance generator (BASELINE configs 3-5) ----------------------
+ * Rows [row0, row0+nrows) of an n x m market: Bernoulli(q_i) support per row
+ * drawn by geometric skipping (q_mode 0: q_i = q; q_mode 1: q_i = d_i/m with a
+ * truncated power-law degree d_i = dmin U^(-1/(alpha-1))), an empty draw
+ * repaired with one uniform column, values and budgets U(0,1].  One Philox
+ * subsequence per row: shards generate independently and identically.
+ * Pass 1 writes per-row degrees; the caller scans them into row_ptr (local,
+ * starting at 0); pass 2 fills columns (ascending), values and budgets (w may
+ * be NULL). */
+int mq_gen_degrees(int64_t row0, int64_t nrows, int64_t m, int q_mode, double q, double alpha,
+                   double dmin, unsigned long long seed, int64_t *deg, void *stream);
+int mq_gen_fill(int64_t row0, int64_t nrows, int64_t m, int q_mode, double q, double alpha,
+                double dmin, unsigned long long seed, const int64_t *row_ptr, int32_t *col,
+                double *val, double *w, void *stream);
+
 /* Size in doubles of the `scratch` buffer the reduction calls need. */
 int64_t mq_scratch_doubles(void);
 

@@ -25,6 +25,7 @@ SOURCES = {
     "abi.cu": [],
     "fast.cu": [],
     "reduce.cu": [],
+    "generate.cu": [],
     "ksection.cu": ["--fmad=false"],
 }
 

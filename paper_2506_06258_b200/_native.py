@@ -45,22 +45,28 @@ class MqState(ctypes.Structure):
                 ("csbar", P), ("steps", P), ("navg", P), ("pass_out", P), ("faults", P)]
 
 
+PM = ctypes.POINTER(MqMarket)
+PS = ctypes.POINTER(MqState)
+
 # name -> (restype, argtypes)
 _SIGS = {
     "mq_pdhcg_chunk": (CINT, [I64, I64, P, P, P, P, P, P, P, P, P, P, P, I64, F64, F64, CINT,
                               F64, CINT, P, P, P, P]),
-    "mq_dual_step": (CINT, [P, P, CINT, P]),
-    "mq_primal_step": (CINT, [P, P, CINT, P, P]),
-    "mq_colsum_step": (CINT, [P, P, CINT, CINT, P]),
-    "mq_colsum_finalize": (CINT, [P, P, CINT, P]),
-    "mq_chunk_end": (CINT, [P, CINT, P]),
-    "mq_fast_chunk": (CINT, [P, P, CINT, P]),
-    "mq_colsum": (CINT, [P, P, P, P]),
-    "mq_resid_rows": (CINT, [P, P, P, CINT, P, P, P, P, P, P]),
+    "mq_dual_step": (CINT, [PM, PS, CINT, P]),
+    "mq_primal_step": (CINT, [PM, PS, CINT, P, P]),
+    "mq_colsum_step": (CINT, [PM, PS, CINT, CINT, P]),
+    "mq_colsum_finalize": (CINT, [PM, PS, CINT, P]),
+    "mq_chunk_end": (CINT, [PS, CINT, P]),
+    "mq_fast_chunk": (CINT, [PM, PS, CINT, P]),
+    "mq_colsum": (CINT, [PM, P, P, P]),
+    "mq_resid_rows": (CINT, [PM, P, P, CINT, P, P, P, P, P, P]),
     "mq_resid_cols": (CINT, [I64, P, P, P, P, P, P]),
-    "mq_restart_moves": (CINT, [P, P, P, P, P, P, P, P, P, P]),
+    "mq_restart_moves": (CINT, [PM, P, P, P, P, P, P, P, P, P]),
     "mq_spmv": (CINT, [I64, P, P, P, P, P, P]),
     "mq_normalize_rows": (CINT, [I64, P, P, P, P, P]),
+    "mq_gen_degrees": (CINT, [I64, I64, I64, CINT, F64, F64, F64, ctypes.c_ulonglong, P, P]),
+    "mq_gen_fill": (CINT, [I64, I64, I64, CINT, F64, F64, F64, ctypes.c_ulonglong, P, P, P, P,
+                           P]),
     "mq_scratch_doubles": (I64, []),
     "mq_last_error": (ctypes.c_char_p, []),
     "mq_abi_version": (CINT, []),

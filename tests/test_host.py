@@ -144,3 +144,39 @@ def test_oracle_not_imported_by_package():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", text, re.M), f
+
+
+def test_abi_marshaling_without_device():
+    """Every entry point accepts its ctypes argument list; without a GPU the
+    CUDA runtime error comes back as a negative code (never a crash)."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("device present: exercised by the gpu tests")
+    from paper_2506_06258_b200 import _native as nat
+
+    lib = nat.load_library()
+    mk, st = nat.MqMarket(), nat.MqState()
+    n64 = ctypes.c_int64(0)
+    calls = {
+        "mq_dual_step": (mk, st, 0, None),
+        "mq_primal_step": (mk, st, 0, None, None),
+        "mq_colsum_step": (mk, st, 0, 1, None),
+        "mq_colsum_finalize": (mk, st, 0, None),
+        "mq_chunk_end": (st, 1, None),
+        "mq_fast_chunk": (mk, st, 1, None),
+        "mq_colsum": (mk, None, None, None),
+        "mq_resid_rows": (mk, None, None, 0, None, None, None, None, None, None),
+        "mq_resid_cols": (0, None, None, None, None, None, None),
+        "mq_restart_moves": (mk, None, None, None, None, None, None, None, None, None),
+        "mq_spmv": (0, None, None, None, None, None, None),
+        "mq_normalize_rows": (0, None, None, None, None, None),
+        "mq_gen_degrees": (0, 1, 10, 0, 0.5, 2.0, 1.0, 1, None, None),
+        "mq_gen_fill": (0, 1, 10, 0, 0.5, 2.0, 1.0, 1, None, None, None, None, None),
+        "mq_pdhcg_chunk": (0, 0, None, None, None, None, None, None, None, None, None, None,
+                           None, 0, 0.1, 0.1, 32, 1e-10, 1, None, None, ctypes.byref(n64), None),
+    }
+    for name, args in calls.items():
+        rc = getattr(lib, name)(*args)
+        assert rc != 0, name
+        assert lib.mq_last_error()
