@@ -21,7 +21,7 @@ import numpy as np
 
 from .adaptive import RestartParams, StepController, should_restart, update_weights
 from .errors import ValidationError
-from .instance import validate
+from .instance import FisherInstance
 from .report import SolveReport, instance_fingerprint
 from .sparse import selector_norm_from_counts
 
@@ -80,6 +80,42 @@ class SolveConfig:
         }
 
 
+class _Fingerprint:
+    """instance_fingerprint computed on a side thread (hashlib releases the
+    GIL on large buffers), overlapped with the device solve."""
+
+    def __init__(self, inst):
+        import threading
+
+        self.value = ""
+        if inst is None:
+            self.thread = None
+            return
+        self.thread = threading.Thread(target=self._run, args=(inst,), daemon=True)
+        self.thread.start()
+
+    def _run(self, inst):
+        self.value = instance_fingerprint(inst)
+
+    def get(self):
+        if self.thread is not None:
+            self.thread.join()
+        return self.value
+
+
+def device_violations(dm):
+    """validate() (instance.py:87-115) evaluated on the device copy."""
+    import torch
+
+    lens = dm.row_ptr[1:] - dm.row_ptr[:-1]
+    out = [f"buyer {int(i)} values no good" for i in torch.nonzero(lens == 0).flatten().tolist()]
+    counts = dm.col_counts
+    out += [f"good {int(j)} unvalued" for j in torch.nonzero(counts == 0).flatten().tolist()]
+    out += [f"nonpositive budget for buyer {int(i)}"
+            for i in torch.nonzero(dm.w <= 0).flatten().tolist()]
+    return out
+
+
 class DeviceSession:
     """Device market + engine kept alive across solves of the same utilities
     (Arrow-Debreu re-solves with new budgets; benchmarks)."""
@@ -96,9 +132,12 @@ class DeviceSession:
         self.op_norm = selector_norm_from_counts(counts)
 
 
-def solve_on_device(session, cfg, warm_start=None, w_sum=None, inst=None, algo="pdhcg"):
+def solve_on_device(session, cfg, warm_start=None, w_sum=None, inst=None, algo="pdhcg",
+                    fingerprint=None):
     """The restarted loop of driver.py:271-377 against a DeviceSession."""
     eng = session.engine
+    if fingerprint is None:
+        fingerprint = _Fingerprint(inst)
     if warm_start is not None:
         x = np.asarray(warm_start["x"], dtype=np.float64)
         p = np.asarray(warm_start["p"], dtype=np.float64)
@@ -181,7 +220,7 @@ def solve_on_device(session, cfg, warm_start=None, w_sum=None, inst=None, algo="
     return SolveReport(
         solver=algo, status=status, inner_iterations=total, restarts=restarts,
         wall_time_seconds=wall, final_residuals=final, residual_history=history,
-        instance_fingerprint=instance_fingerprint(inst) if inst is not None else "",
+        instance_fingerprint=fingerprint.get(),
         config_echo=echo, subproblem_passes=passes, objective=objective,
         device_stats={"chunk_seconds": chunk_time,
                       "iters_per_second": total / chunk_time if chunk_time > 0 else None,
@@ -196,13 +235,16 @@ def run_solve(inst, cfg, algo, warm_start=None):
     "p": prices}.  Only algo="pdhcg" is provided (lifted PDHG is out of scope
     for this hot path).
     """
-    violations = validate(inst)
-    if violations:
-        raise ValidationError("; ".join(violations))
     if algo != "pdhcg":
         if algo == "pdhg":
             raise NotImplementedError("lifted PDHG is not part of the B200 hot path yet")
         raise ValueError(f"unknown algorithm {algo!r}")
+    if not isinstance(inst, FisherInstance):
+        raise TypeError(f"unsupported instance type {type(inst)!r}")
+    fp = _Fingerprint(inst)
     session = DeviceSession(inst, cfg)
+    violations = device_violations(session.dm)
+    if violations:
+        raise ValidationError("; ".join(violations))
     return solve_on_device(session, cfg, warm_start=warm_start,
-                           w_sum=float(np.sum(inst.budgets)), inst=inst)
+                           w_sum=float(np.sum(inst.budgets)), inst=inst, fingerprint=fp)
