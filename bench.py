@@ -328,8 +328,8 @@ def main():
     value = a.steps / (t_ms / 1e3)
     # kernels launched in the timed region: dual + non-empty primal bins + colsum
     # per iteration, chunk_end per chunk (+ finalize on N>1)
-    bins = int(np.count_nonzero(np.diff(dm.bin_off)))
-    per_it = 2 + bins + (1 if world > 1 else 0)
+    primal_kernels = int(dm.tiles.shape[0] > 0) + int(dm.long_rows.numel() > 0)
+    per_it = 2 + primal_kernels + (1 if world > 1 else 0)
     launches = a.steps * per_it + -(-a.steps // 40)
 
     # per-kernel breakdown and the primal kernel's roofline

@@ -33,21 +33,40 @@ extern "C" {
 #endif
 
 #define MQ_ABI_VERSION 1
-#define MQ_NBINS 9 /* row-length bins of the fast primal kernel */
+#define MQ_TILE_ENTRIES 2048 /* entries staged per shared-memory tile      */
+#define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
+#define MQ_TILE_ROWS 256      /* rows per tile                                */
 
-/* Read-only market description (device pointers, borrowed). */
+/* Read-only market description (device pointers, borrowed).  Arrays marked
+ * [pad] must have 16 readable bytes past their last element (TMA bulk copies
+ * move 16-byte-aligned ranges). */
 typedef struct mq_market {
     int64_t n, m, nnz;
-    const int64_t *row_ptr;  /* [n+1]                                          */
-    const int32_t *col;      /* [nnz] strictly increasing within a row         */
-    const double *u;         /* [nnz] normalized utilities (row max 1),
+    const int64_t *row_ptr;  /* [n+1] [pad]                                    */
+    const int32_t *col;      /* [nnz] [pad] strictly increasing within a row   */
+    const double *u;         /* [nnz] [pad] normalized utilities (row max 1),
                                 instance.py:118-138                             */
     const double *u_orig;    /* [nnz] original utilities (residuals, kkt.py)    */
-    const double *w;         /* [n] budgets                                     */
-    const int64_t *tptr;     /* [m+1] column offsets of the transpose schedule  */
-    const int32_t *tperm;    /* [nnz] storage positions grouped by column       */
-    const int32_t *bin_rows; /* [n] row ids grouped by length bin (fast path)   */
-    int64_t bin_off[MQ_NBINS + 1]; /* host-side offsets into bin_rows          */
+    const double *w;         /* [n] [pad] budgets                               */
+    /* row tiles of the primal kernel: tile k = rows [tiles[2k], tiles[2k+1]),
+       at most MQ_TILE_ENTRIES entries and MQ_TILE_ROWS rows, no row longer
+       than MQ_LONG_ROW                                                       */
+    const int64_t *tiles;
+    int64_t ntiles;
+    const int32_t *long_rows; /* rows longer than MQ_LONG_ROW                   */
+    int64_t nlong;
+    /* tile-blocked transpose schedule for the fused column sums: the tiles
+       are grouped in blocks of tiles_per_block consecutive tiles (block b is
+       finished once the persistent grid of prim_grid CTAs has solved it);
+       bperm lists, block by block and column by column, the entry positions
+       of each block (ascending inside a column), bptr[b*m + j] where
+       (block b, good j) starts; pseudo-block nblk holds the long rows'
+       entries.  Walking a good's segments over b = 0..nblk visits its tile
+       entries in ascending row order.                                        */
+    const int32_t *bperm;    /* [nnz]                                           */
+    const int32_t *bptr;     /* [(nblk+1)*m + 1]                                */
+    int64_t nblk, tiles_per_block;
+    int32_t prim_grid;       /* CTAs of the persistent primal kernel            */
     int64_t row_begin;       /* first global row of this shard (0 on 1 GPU)    */
 } mq_market;
 
@@ -56,13 +75,15 @@ typedef struct mq_market {
  * needs colsum(2x^k - x^{k-1}) = 2 cs - cs_prev, so x^{k-1} itself is never
  * stored. */
 typedef struct mq_state {
-    double *x;        /* [nnz] current allocation x^k (updated in place)      */
-    double *xbar;     /* [nnz] running average                                 */
+    double *x;        /* [nnz] [pad] current allocation x^k (updated in place) */
+    double *xbar;     /* [nnz] [pad] running average                           */
     double *p;        /* [m]   prices                                          */
     double *pbar;     /* [m]   running average of prices                       */
     double *cs;       /* [m]   colsum(x^k)                                     */
     double *cs_prev;  /* [m]   colsum(x^{k-1})                                 */
     double *csbar;    /* [m]   colsum(xbar)                                    */
+    int32_t *blk_done;/* [2*nblk] per block: tiles solved, column-sum warps done
+                         (zeroed per launch)                                   */
     const double *steps; /* [2] tau, sigma (device-resident: one graph serves
                             every step size)                                   */
     int64_t *navg;    /* [1]  inner iterations since the last restart          */
@@ -91,20 +112,22 @@ int mq_pdhcg_chunk(int64_t n, int64_t m, const int64_t *indptr, const int32_t *c
  * p += sigma (2 cs - cs_prev - 1); pbar <- avg; cs_prev <- cs. */
 int mq_dual_step(const mq_market *mk, const mq_state *st, int it, void *stream);
 
-/* Exact per-buyer proximal step fused with the allocation average
- * (kernels.py:117-142): for every row, the unique root s of
- * s = sum_j u_j max(0, c_j + tau w u_j / s), c = x - tau p[col], by the
- * monotone active-set iteration (closed-form root per active set), then
- * x <- max(0, c + tau w u / s), xbar <- avg.  x_prev_out (may be NULL)
- * receives the pre-step x (the reference's x_prev copy).
- * pass_out[it] += number of active-set sweeps. */
+/* Exact per-buyer proximal step fused with the allocation average and the
+ * column sums (kernels.py:117-142 then the next iteration's 111-116): for
+ * every row, the unique root s of s = sum_j u_j max(0, c_j + tau w u_j / s),
+ * c = x - tau p[col], by the monotone active-set iteration (closed-form root
+ * per active set), then x <- max(0, c + tau w u / s), xbar <- avg; the
+ * kernel's column-sum warps gather each finished block of x from L2 into
+ * cs = colsum(x) over the tile rows (deterministic: one thread per good,
+ * blocks in order).  x_prev_out (may be NULL) receives the pre-step x (the
+ * reference's x_prev copy).  pass_out[it] += number of active-set sweeps. */
 int mq_primal_step(const mq_market *mk, const mq_state *st, int it, double *x_prev_out,
                    void *stream);
 
-/* cs <- colsum(x) over this shard's rows in the fixed ascending-row order of
- * the transpose schedule (deterministic, no atomics).  With finalize != 0
- * (single GPU) also csbar <- avg(csbar, cs); multi-GPU callers allreduce cs
- * first and then call mq_colsum_finalize. */
+/* Completes cs = colsum(x) over this shard: adds the long rows' entries (the
+ * pseudo-block of the schedule) to the tile sums of mq_primal_step.  With
+ * finalize != 0 (single GPU) also csbar <- avg(csbar, cs); multi-GPU callers
+ * allreduce cs first and then call mq_colsum_finalize. */
 int mq_colsum_step(const mq_market *mk, const mq_state *st, int it, int finalize,
                    void *stream);
 int mq_colsum_finalize(const mq_market *mk, const mq_state *st, int it, void *stream);
@@ -115,7 +138,8 @@ int mq_chunk_end(const mq_state *st, int iters, void *stream);
 /* Whole chunk on one GPU: `iters` x (dual, primal, colsum) + chunk_end. */
 int mq_fast_chunk(const mq_market *mk, const mq_state *st, int iters, void *stream);
 
-/* Plain column sums out[j] = sum_{col j} v (fixed order), e.g. colsum(x0). */
+/* Plain column sums out[j] = sum_{col j} v over this shard, one thread per
+ * good walking the blocked schedule (ascending rows; deterministic). */
 int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream);
 
 /* ---- residuals (kkt.py:29-87 specialised to the compact state) -----------

@@ -39,14 +39,18 @@ def _sources_newer_than_lib():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, extra_flags=(), out=None):
+    target = out or LIB
+    if out is None and os.environ.get("MQ_LIB"):
+        return os.environ["MQ_LIB"]  # a prebuilt variant was selected
     if not force and not _sources_newer_than_lib():
         return LIB
     with tempfile.TemporaryDirectory() as tmp:
         objs = []
         for src, extra in SOURCES.items():
             obj = os.path.join(tmp, src + ".o")
-            cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+            cmd = [NVCC, *ARCH, *COMMON, *extra, *extra_flags, "-c", os.path.join(CSRC, src),
+                   "-o", obj]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
                 print(" ".join(cmd), flush=True)
@@ -56,10 +60,11 @@ def build(force=False, verbose=False):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", tmp_lib, *objs,
                "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         subprocess.run(cmd, check=True)
-        os.replace(tmp_lib, LIB)
-    return LIB
+        os.replace(tmp_lib, target)
+    return target
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="--verbose" in sys.argv)
+    flags = ["-DMQ_PROFILE_WAITS"] if "--profile-waits" in sys.argv else []
+    build(force=True, verbose="--verbose" in sys.argv, extra_flags=flags)
     print(LIB)

@@ -12,8 +12,11 @@ import threading
 from .errors import MarketError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmarket_eq_b200.so")
-NBINS = 9
+LIB_PATH = os.environ.get("MQ_LIB") or os.path.join(_PKG, "libmarket_eq_b200.so")
+TILE_ENTRIES = 2048   # MQ_TILE_ENTRIES
+LONG_ROW = 1024       # MQ_LONG_ROW
+TILE_ROWS = 256       # MQ_TILE_ROWS
+PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
 ABI_VERSION = 1
 
 _lock = threading.Lock()
@@ -36,13 +39,15 @@ class NativeError(MarketError, RuntimeError):
 class MqMarket(ctypes.Structure):
     _fields_ = [("n", I64), ("m", I64), ("nnz", I64),
                 ("row_ptr", P), ("col", P), ("u", P), ("u_orig", P), ("w", P),
-                ("tptr", P), ("tperm", P), ("bin_rows", P),
-                ("bin_off", I64 * (NBINS + 1)), ("row_begin", I64)]
+                ("tiles", P), ("ntiles", I64), ("long_rows", P), ("nlong", I64),
+                ("bperm", P), ("bptr", P), ("nblk", I64), ("tiles_per_block", I64),
+                ("prim_grid", ctypes.c_int32), ("row_begin", I64)]
 
 
 class MqState(ctypes.Structure):
     _fields_ = [("x", P), ("xbar", P), ("p", P), ("pbar", P), ("cs", P), ("cs_prev", P),
-                ("csbar", P), ("steps", P), ("navg", P), ("pass_out", P), ("faults", P)]
+                ("csbar", P), ("blk_done", P), ("steps", P), ("navg", P), ("pass_out", P),
+                ("faults", P)]
 
 
 PM = ctypes.POINTER(MqMarket)

@@ -12,12 +12,34 @@
 // closed-form root; starting from any lower bound of the root, the
 // re-evaluated active set can only shrink and the root only grow, so the
 // iteration is monotone and ends, exactly, when the set stops changing.
+//
+// One persistent, warp-specialized kernel per iteration (primal_fused_kernel):
+//  * a TMA producer warp streams each tile (whole rows, <= MQ_TILE_ENTRIES
+//    entries: u, col, x, xbar, row offsets, budgets) into a 3-stage
+//    shared-memory ring with cp.async.bulk + mbarrier transaction counts;
+//  * 16 solver warps claim row pairs of the current tile (two 16-lane groups
+//    per warp) and solve them from shared memory, writing x and xbar;
+//  * 4 column-sum warps gather, block by block, the freshly written x of
+//    every finished block of tiles from L2 (one thread per good, ascending
+//    rows, fixed order), so the price step's column sums cost no extra HBM
+//    pass and overlap the streaming.
 #include "mq_common.cuh"
 
 namespace mq {
 
-constexpr int kPrimalThreads = 256;
 constexpr int kMaxSweeps = 4096;
+
+// cycle counters of the fused kernel's waits (mq_debug_counters): 0 solver
+// waiting for a tile, 1 solver throttled, 2 producer waiting for a free stage,
+// 3 column-sum warps waiting for a block, 4 column-sum gather cycles
+__device__ unsigned long long g_wait_cycles[8];
+#ifdef MQ_PROFILE_WAITS
+#define MQ_T0() const long long _t0 = clock64()
+#define MQ_T1(slot) atomicAdd(&g_wait_cycles[slot], (unsigned long long)(clock64() - _t0))
+#else
+#define MQ_T0()
+#define MQ_T1(slot)
+#endif
 
 struct Avg {
     double wold, wnew;
@@ -28,6 +50,43 @@ __device__ __forceinline__ Avg avg_weights(const int64_t *navg, int it) {
     a.wold = ((double)count - 1.0) / (double)count;
     a.wnew = 1.0 / (double)count;
     return a;
+}
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "MQ_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra MQ_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // ------------------------------------------------------------ price step
@@ -48,138 +107,467 @@ __global__ void dual_kernel(int64_t m, double *__restrict__ p, double *__restric
     }
 }
 
-// ------------------------------------------------------------ primal step
-// One G-lane group per row, PER entries per lane held in registers.
-template <int G, int PER>
-__global__ void __launch_bounds__(kPrimalThreads)
-primal_group_kernel(const mq_market mk, const mq_state st, int it,
-                    double *__restrict__ x_prev_out, int64_t bin_lo, int64_t bin_hi) {
-    constexpr int GPW = 32 / G;
-    const int lane = threadIdx.x & (G - 1);
-    const int gsub = (threadIdx.x & 31) / G;
-    const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const double tau = st.steps[0];
-    const Avg av = avg_weights(st.navg, it);
-    const double *__restrict__ U = mk.u;
-    const int32_t *__restrict__ COL = mk.col;
-    const double *__restrict__ P = st.p;
-    double *__restrict__ X = st.x;
-    double *__restrict__ XB = st.xbar;
-    int64_t my_sweeps = 0;
-    int my_faults = 0;
-
-    for (int64_t base = bin_lo + warp_id * GPW; base < bin_hi; base += nwarps * GPW) {
-        const int64_t r = base + gsub;
-        const bool has_row = r < bin_hi;
-        int64_t a = 0, b = 0;
-        double tw = 0.0;
-        if (has_row) {
-            const int64_t i = mk.bin_rows[r];
-            a = mk.row_ptr[i];
-            b = mk.row_ptr[i + 1];
-            tw = tau * mk.w[i];
-        }
-        double c[PER], u[PER];
-        double s0p = 0.0, ap = 0.0, bp = 0.0;
-#pragma unroll
-        for (int e = 0; e < PER; ++e) {
-            const int64_t t = a + lane + (int64_t)e * G;
-            if (t < b) {
-                const double ue = __ldg(U + t);
-                const double xe = X[t];
-                const double pe = __ldg(P + __ldg(COL + t));
-                if (x_prev_out) x_prev_out[t] = xe;
-                u[e] = ue;
-                c[e] = xe - tau * pe;
-                s0p += ue * xe;
-                ap += ue * c[e];
-                bp += ue * ue;
-            } else {
-                u[e] = 0.0;
-                c[e] = 0.0;
+// ------------------------------------------------------------ row solve
+// Exact root of s = sum_t u_t max(0, c_t + tw u_t / s) for one row held in
+// shared memory (u, c), by a G-lane group.  All groups of a warp call this
+// together (warp-uniform loops around the shuffles).  Returns s; *sweeps gets
+// the number of active-set evaluations, *ok whether it converged.
+template <int G>
+__device__ __forceinline__ double row_root_exact(const double *__restrict__ su,
+                                                 const double *__restrict__ sc, int a, int b,
+                                                 int lane, double tw, double s0, double A,
+                                                 double B, bool active_row, int *sweeps,
+                                                 bool *ok) {
+    const int len = b - a;
+    bool done = !active_row || len == 0;
+    double s = done ? 1.0 : active_root(A, B, tw);  // all entries active: lower bound
+    int prev_cnt = len;
+    int nsw = 0;
+    auto sweep = [&](double q, double &As, double &Bs, int &cnt) {
+        double a_ = 0.0, b_ = 0.0;
+        int k_ = 0;
+        for (int t = a + lane; t < b; t += G) {
+            const double ue = su[t], ce = sc[t];
+            if (fma(ce, q, tw * ue) > 0.0) {
+                a_ += ue * ce;
+                b_ += ue * ue;
+                ++k_;
             }
         }
-        const double s0 = group_sum<G>(s0p);
-        const double A = group_sum<G>(ap);
-        const double B = group_sum<G>(bp);
-        const int len = (int)(b - a);
-        bool done = !has_row || len == 0;
-
-        // lower bound: root with every entry active (its h(s) <= g(s))
-        double s = done ? 1.0 : active_root(A, B, tw);
-        int prev_cnt = len;
-        int sweeps = 0;
-
-        auto sweep = [&](double q, double &As, double &Bs, int &cnt) {
-            double a_ = 0.0, b_ = 0.0;
-            int k_ = 0;
-#pragma unroll
-            for (int e = 0; e < PER; ++e) {
-                if (fma(c[e], q, tw * u[e]) > 0.0 && u[e] > 0.0) {
-                    a_ += u[e] * c[e];
-                    b_ += u[e] * u[e];
-                    ++k_;
-                }
-            }
-            As = group_sum<G>(a_);
-            Bs = group_sum<G>(b_);
-            cnt = group_sum_int<G>(k_);
-        };
-
-        // the previous iterate's utility s0 is usually next to the root
-        const bool try_s0 = !done && s0 > s;
-        if (__any_sync(MQ_FULL, try_s0)) {
-            double A0, B0;
-            int k0;
-            sweep(try_s0 ? s0 : s, A0, B0, k0);
-            if (try_s0) {
-                ++sweeps;
-                const double g0 = A0 + tw * B0 / s0;
-                if (g0 >= s0) {          // s0 below the root: step from its set
-                    s = fmax(active_root(A0, B0, tw), s0);
-                    prev_cnt = k0;
-                } else if (g0 > s) {     // g(s0) is a lower bound above s
-                    s = g0;
-                    prev_cnt = -1;
-                }
-            }
-        }
-        for (int k = 0; k < kMaxSweeps; ++k) {
-            if (!__any_sync(MQ_FULL, !done)) break;
-            double As, Bs;
-            int cnt;
-            sweep(s, As, Bs, cnt);
-            if (!done) {
-                ++sweeps;
-                if (cnt == prev_cnt || cnt == 0) {
-                    done = true;  // s is the root of its own active set
-                } else {
-                    s = fmax(active_root(As, Bs, tw), s);
-                    prev_cnt = cnt;
-                }
-            }
-        }
-        if (has_row && len > 0 && lane == 0) {
-            my_sweeps += sweeps;
-            if (!done) ++my_faults;
-        }
-        const double inv_s = 1.0 / s;
-#pragma unroll
-        for (int e = 0; e < PER; ++e) {
-            const int64_t t = a + lane + (int64_t)e * G;
-            if (t < b) {
-                const double xn = fmax(c[e] + tw * u[e] * inv_s, 0.0);
-                X[t] = xn;
-                XB[t] = av.wold * XB[t] + av.wnew * xn;
+        As = group_sum<G>(a_);
+        Bs = group_sum<G>(b_);
+        cnt = group_sum_int<G>(k_);
+    };
+    // the previous iterate's utility s0 is usually next to the new root
+    const bool try_s0 = !done && s0 > s;
+    if (__any_sync(MQ_FULL, try_s0)) {
+        double A0, B0;
+        int k0;
+        sweep(try_s0 ? s0 : s, A0, B0, k0);
+        if (try_s0) {
+            ++nsw;
+            const double g0 = A0 + tw * B0 / s0;
+            if (g0 >= s0) {  // s0 below the root: step from its active set
+                s = fmax(active_root(A0, B0, tw), s0);
+                prev_cnt = k0;
+            } else if (g0 > s) {  // g(s0) is a lower bound above s
+                s = g0;
+                prev_cnt = -1;
             }
         }
     }
-    __shared__ int64_t red[32];
-    const int64_t tot = block_sum_i64(my_sweeps, red);
-    if (threadIdx.x == 0 && tot) atomicAdd((unsigned long long *)(st.pass_out + it), (unsigned long long)tot);
-    const int64_t fl = block_sum_i64((int64_t)my_faults, red);
-    if (threadIdx.x == 0 && fl) atomicAdd((unsigned long long *)st.faults, (unsigned long long)fl);
+    for (int k = 0; k < kMaxSweeps; ++k) {
+        if (!__any_sync(MQ_FULL, !done)) break;
+        double As, Bs;
+        int cnt;
+        sweep(s, As, Bs, cnt);
+        if (!done) {
+            ++nsw;
+            if (cnt == prev_cnt || cnt == 0) {
+                done = true;  // s is the root of its own active set
+            } else {
+                s = fmax(active_root(As, Bs, tw), s);
+                prev_cnt = cnt;
+            }
+        }
+    }
+    *sweeps = nsw;
+    *ok = done;
+    return s;
+}
+
+// ------------------------------------------------------------ primal (fused)
+template <int ETILE, int RTILE>
+struct TileLayout {
+    // one stage (every region 16-byte aligned for the bulk copies):
+    // u, x, xbar f64 [ETILE+2] | col i32 [ETILE+4] | row_ptr i64 [RTILE+4] | w f64 [RTILE+2]
+    static constexpr int kU = 0;
+    static constexpr int kX = kU + (ETILE + 2) * 8;
+    static constexpr int kXB = kX + (ETILE + 2) * 8;
+    static constexpr int kCol = kXB + (ETILE + 2) * 8;
+    static constexpr int kRp = kCol + (ETILE + 4) * 4;
+    static constexpr int kW = kRp + (RTILE + 4) * 8;
+    static constexpr int kStage = (kW + (RTILE + 2) * 8 + 127) / 128 * 128;
+    static_assert(kX % 16 == 0 && kCol % 16 == 0 && kRp % 16 == 0 && kW % 16 == 0,
+                  "bulk-copy destinations must be 16-byte aligned");
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes,
+                                              uint64_t *bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// 16-byte-aligned superset of [first, first+count) elements of size S
+template <int S>
+__device__ __forceinline__ void aligned_span(const void *base, int64_t first, int64_t count,
+                                             const unsigned char **src, uint32_t *bytes) {
+    const uint32_t d = (uint32_t)((first * S) & 15);
+    *src = reinterpret_cast<const unsigned char *>(base) + first * S - d;
+    *bytes = (uint32_t)((d + count * S + 15) & ~(int64_t)15);
+}
+
+constexpr int kCsCap = 10240;         // staged bperm entries per CTA (40 KB)
+constexpr int kCsCols = 1152;         // goods per CTA (>= QMAX * NCW * 32)
+#ifndef MQ_LAG
+#define MQ_LAG 4
+#endif
+constexpr int64_t kLag = MQ_LAG;      // solver blocks ahead of the slowest column-sum CTA
+constexpr int64_t kSpinLimit = 4000000000ll;  // ~2 s of clock64: a stalled block is a fault
+
+// named barrier among the NCW column-sum warps (id 1; __syncthreads uses 0)
+__device__ __forceinline__ void colsum_sync(int ncw) {
+    asm volatile("bar.sync 1, %0;" ::"r"(ncw * 32) : "memory");
+}
+
+__device__ __forceinline__ int ld_relaxed(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// spin (one lane) until *ctr >= target with relaxed loads (an acquiring load
+// would invalidate L1 on every poll), then one acquire fence if the caller
+// reads data published before the counter; a stall past kSpinLimit is a fault
+__device__ __forceinline__ void wait_counter(const int *ctr, int target, int64_t *faults,
+                                             bool acquire) {
+    if (ld_relaxed(ctr) < target) {
+        const long long t0 = clock64();
+        while (ld_relaxed(ctr) < target) {
+            __nanosleep(200);
+            if (clock64() - t0 > kSpinLimit) {
+                atomicAdd((unsigned long long *)faults, 1ull << 40);
+                break;
+            }
+        }
+    }
+    if (acquire) __threadfence();
+}
+
+// Warps 0..NSW-1 solve rows, warp NSW produces (TMA), warps NSW+1..NSW+NCW sum
+// columns.  full[s]: stage s has landed; empty[s]: every solver warp is done
+// with it.  Solver warps claim row pairs from a shared counter, so no solver
+// waits for another inside a tile.
+template <int G, int NSW, int NCW, int ETILE, int RTILE, int NSTAGE, int QMAX>
+__global__ void __launch_bounds__((NSW + NCW + 1) * 32, 1)
+primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
+                    int write_cs) {
+    using L = TileLayout<ETILE, RTILE>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTAGE * L::kStage);
+    uint64_t *empty = full + NSTAGE;
+    int *claim = reinterpret_cast<int *>(empty + NSTAGE);
+    int32_t *cstage = reinterpret_cast<int32_t *>(claim + 4 * NSTAGE);  // column-sum staging
+    constexpr int GPW = 32 / G;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, wl = tid & 31;
+    const int64_t first = blockIdx.x, stride = gridDim.x;
+    const int64_t tpb_all = mk.tiles_per_block;  // tiles per block (all CTAs)
+
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NSW);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    if (warp == NSW) {  // ---------------------------------------- producer
+        if (wl == 0) {
+            const uint64_t pol = policy_evict_first();
+            auto finished = [&](int64_t k) {  // tile k fully written by this CTA
+                __threadfence();
+                atomicAdd(&st.blk_done[k / tpb_all], 1);
+            };
+            int64_t j = 0;
+            for (;; ++j) {
+                const int64_t k = first + j * stride;
+                if (k >= mk.ntiles) break;
+                const int s = (int)(j % NSTAGE);
+                if (j >= NSTAGE) {
+                    MQ_T0();
+                    mbar_wait(&empty[s], (uint32_t)(((j / NSTAGE) - 1) & 1));
+                    MQ_T1(2);
+                    finished(first + (j - NSTAGE) * stride);
+                }
+                claim[s] = 0;
+                fence_proxy_async();
+                const int64_t r0 = mk.tiles[2 * k], r1 = mk.tiles[2 * k + 1];
+                const int64_t e0 = mk.row_ptr[r0], cnt = mk.row_ptr[r1] - e0;
+                unsigned char *base = smem + s * L::kStage;
+                const unsigned char *src_rp, *src_w, *src_u, *src_x, *src_xb, *src_c;
+                uint32_t brp, bw, b8 = 0, b4 = 0;
+                aligned_span<8>(mk.row_ptr, r0, r1 - r0 + 1, &src_rp, &brp);
+                aligned_span<8>(mk.w, r0, r1 - r0, &src_w, &bw);
+                aligned_span<8>(mk.u, e0, cnt, &src_u, &b8);
+                aligned_span<8>(st.x, e0, cnt, &src_x, &b8);
+                aligned_span<8>(st.xbar, e0, cnt, &src_xb, &b8);
+                aligned_span<4>(mk.col, e0, cnt, &src_c, &b4);
+                mbar_expect_tx(&full[s], brp + bw + (cnt > 0 ? 3 * b8 + b4 : 0));
+                bulk_g2s(base + L::kRp, src_rp, brp, &full[s]);
+                bulk_g2s(base + L::kW, src_w, bw, &full[s]);
+                if (cnt > 0) {
+                    bulk_g2s_hint(base + L::kU, src_u, b8, &full[s], pol);
+                    bulk_g2s(base + L::kX, src_x, b8, &full[s]);
+                    bulk_g2s_hint(base + L::kXB, src_xb, b8, &full[s], pol);
+                    bulk_g2s_hint(base + L::kCol, src_c, b4, &full[s], pol);
+                }
+            }
+            // drain: the last (up to NSTAGE) tiles
+            for (int64_t jj = (j > NSTAGE ? j - NSTAGE : 0); jj < j; ++jj) {
+                const int s = (int)(jj % NSTAGE);
+                mbar_wait(&empty[s], (uint32_t)((jj / NSTAGE) & 1));
+                finished(first + jj * stride);
+            }
+        }
+        return;
+    }
+
+    if (warp > NSW) {  // ---------------------------------------- column sums
+        // The CTA's NCW column-sum warps own goods [j_lo, j_hi); thread ct owns
+        // j_lo + ct + q*NCW*32.  Per block, one thread stages the block's
+        // schedule slice (bptr for the owned goods, their bperm range) into
+        // shared memory with TMA bulk copies, issued before the block is even
+        // solved; once every CTA has solved the block, each thread gathers its
+        // goods' x values from L2 and adds them in ascending row order.
+        const int ct = tid - (NSW + 1) * 32;
+        const int64_t per = (mk.m + gridDim.x - 1) / gridDim.x;
+        const int64_t j_lo = blockIdx.x * per;
+        const int64_t j_hi = j_lo + per < mk.m ? j_lo + per : mk.m;
+        const int nc = (int)(j_hi > j_lo ? j_hi - j_lo : 0);
+        int32_t *sperm = cstage;
+        int32_t *sbptr = cstage + kCsCap;
+        int64_t *meta = reinterpret_cast<int64_t *>(sbptr + kCsCols + 8);  // rlo, rhi, lead
+        uint64_t *cbar = reinterpret_cast<uint64_t *>(meta + 4);
+        if (ct == 0) {
+            mbar_init(cbar, 1);
+            mbar_fence_init();
+        }
+        colsum_sync(NCW);
+        if (nc == 0) {  // no goods here: still publish progress for the throttle
+            if (ct == 0)
+                for (int64_t b = 0; b < mk.nblk; ++b) atomicAdd(st.blk_done + mk.nblk + b, 1);
+            return;
+        }
+        uint32_t cphase = 0;
+        // stage chunk [c0, c1) of block b's bperm range (+ the bptr slice on c0 == rlo)
+        auto stage = [&](int64_t b, int64_t c0, bool with_ptr) {
+            const unsigned char *src;
+            uint32_t bytes_p = 0, bytes_b = 0;
+            const int64_t row0 = b * mk.m;
+            if (with_ptr) {
+                const int64_t rlo = __ldg(mk.bptr + row0 + j_lo), rhi = __ldg(mk.bptr + row0 + j_hi);
+                meta[0] = rlo;
+                meta[1] = rhi;
+                c0 = rlo;
+            }
+            const int64_t c1 = c0 + kCsCap - 4 < meta[1] ? c0 + kCsCap - 4 : meta[1];
+            meta[2] = c0;
+            meta[3] = c1;
+            const unsigned char *srcp;
+            aligned_span<4>(mk.bperm, c0, c1 - c0, &srcp, &bytes_p);
+            if (with_ptr) aligned_span<4>(mk.bptr, row0 + j_lo, nc + 1, &src, &bytes_b);
+            mbar_expect_tx(cbar, (c1 > c0 ? bytes_p : 0) + bytes_b);
+            if (c1 > c0) bulk_g2s(sperm, srcp, bytes_p, cbar);
+            if (with_ptr) bulk_g2s(sbptr, src, bytes_b, cbar);
+        };
+        double acc[QMAX];
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) acc[q] = 0.0;
+        if (ct == 0) stage(0, 0, true);
+        for (int64_t b = 0; b < mk.nblk; ++b) {
+            const int64_t kb0 = b * tpb_all;
+            const int target = (int)((kb0 + tpb_all < mk.ntiles ? kb0 + tpb_all : mk.ntiles) - kb0);
+            {
+                MQ_T0();
+                if (ct == 0) wait_counter(st.blk_done + b, target, st.faults, true);
+                colsum_sync(NCW);
+                if (ct == 0) MQ_T1(3);
+            }
+            MQ_T0();
+            const int bl = (int)((((b * mk.m + j_lo) * 4) & 15) >> 2);  // lead of the bptr slice
+            for (;;) {
+                mbar_wait(cbar, cphase);
+                cphase ^= 1u;
+                const int64_t c0 = meta[2], c1 = meta[3], rhi = meta[1];
+                const int pl = (int)(((c0 * 4) & 15) >> 2);
+                const int32_t *sp = sperm + pl;
+#pragma unroll
+                for (int q = 0; q < QMAX; ++q) {
+                    const int jl = ct + q * NCW * 32;
+                    if (jl >= nc) break;
+                    int64_t t = sbptr[bl + jl], e = sbptr[bl + jl + 1];
+                    t = t > c0 ? t : c0;
+                    e = e < c1 ? e : c1;
+                    double a = acc[q];
+                    for (; t + 8 <= e; t += 8) {
+                        const int32_t *q8 = sp + (t - c0);
+                        double v[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) v[u] = __ldcg(st.x + q8[u]);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) a += v[u];
+                    }
+                    if (t < e) {  // tail: up to 7 loads in flight, added in order
+                        double v[7];
+                        const int n_t = (int)(e - t);
+#pragma unroll
+                        for (int u = 0; u < 7; ++u)
+                            v[u] = u < n_t ? __ldcg(st.x + sp[t - c0 + u]) : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 7; ++u)
+                            if (u < n_t) a += v[u];
+                    }
+                    acc[q] = a;
+                }
+                colsum_sync(NCW);  // everyone is done with the staged chunk
+                if (c1 >= rhi) break;
+                if (ct == 0) {
+                    fence_proxy_async();
+                    stage(b, c1, false);
+                }
+            }
+            if (ct == 0) {
+                MQ_T1(4);
+                atomicAdd(st.blk_done + mk.nblk + b, 1);  // block b gathered by this CTA
+                if (b + 1 < mk.nblk) {
+                    fence_proxy_async();
+                    stage(b + 1, 0, true);
+                }
+            }
+        }
+        if (write_cs) {
+#pragma unroll
+            for (int q = 0; q < QMAX; ++q) {
+                const int jl = ct + q * NCW * 32;
+                if (jl < nc) st.cs[j_lo + jl] = acc[q];
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- solvers
+    const int lane = tid & (G - 1);
+    const int gsub = wl / G;
+    const double tau = st.steps[0];
+    const Avg av = avg_weights(st.navg, it);
+    int64_t my_sweeps = 0;
+    int64_t my_faults = 0;
+    for (int64_t j = 0;; ++j) {
+        const int64_t k = first + j * stride;
+        if (k >= mk.ntiles) break;
+        const int s = (int)(j % NSTAGE);
+        // throttle: stay within kLag blocks of the column-sum front, so the
+        // blocks still to be gathered are L2-resident
+        const int64_t blk = k / tpb_all;
+        {
+            MQ_T0();
+            if (blk >= kLag && wl == 0)
+                wait_counter(st.blk_done + mk.nblk + (blk - kLag), (int)gridDim.x, st.faults,
+                             false);
+            __syncwarp();
+            if (wl == 0) MQ_T1(1);
+        }
+        {
+            MQ_T0();
+            mbar_wait(&full[s], (uint32_t)((j / NSTAGE) & 1));
+            if (wl == 0) MQ_T1(0);
+        }
+        const int64_t r0 = mk.tiles[2 * k], r1 = mk.tiles[2 * k + 1];
+        const int nrows = (int)(r1 - r0);
+        unsigned char *base = smem + s * L::kStage;
+        const int lr = (int)(((r0 * 8) & 15) >> 3);
+        const int64_t *srp = reinterpret_cast<const int64_t *>(base + L::kRp) + lr;
+        const double *sw = reinterpret_cast<const double *>(base + L::kW) + lr;
+        const int64_t e0 = srp[0];
+        const int d8 = (int)(((e0 * 8) & 15) >> 3), d4 = (int)(((e0 * 4) & 15) >> 2);
+        const double *su = reinterpret_cast<const double *>(base + L::kU) + d8;
+        double *sx = reinterpret_cast<double *>(base + L::kX) + d8;  // x, then c in place
+        const double *sxb = reinterpret_cast<const double *>(base + L::kXB) + d8;
+        const int32_t *scol = reinterpret_cast<const int32_t *>(base + L::kCol) + d4;
+
+        for (;;) {
+            int rb = 0;
+            if (wl == 0) rb = atomicAdd(&claim[s], GPW);
+            rb = __shfl_sync(MQ_FULL, rb, 0);
+            if (rb >= nrows) break;  // warp-uniform
+            const int r = rb + gsub;
+            const bool has = r < nrows;
+            int a = 0, b = 0;
+            double tw = 0.0;
+            if (has) {
+                a = (int)(srp[r] - e0);
+                b = (int)(srp[r + 1] - e0);
+                tw = tau * sw[r];
+            }
+            MQ_T0();
+            double s0p = 0.0, ap = 0.0, bp = 0.0;
+            for (int t = a + lane; t < b; t += G) {
+                const double ue = su[t], xe = sx[t];
+                const double ce = xe - tau * __ldg(st.p + scol[t]);
+                if (x_prev_out) x_prev_out[e0 + t] = xe;
+                sx[t] = ce;
+                s0p += ue * xe;
+                ap += ue * ce;
+                bp += ue * ue;
+            }
+            const double s0 = group_sum<G>(s0p);
+            const double A = group_sum<G>(ap);
+            const double B = group_sum<G>(bp);
+            if (wl == 0) MQ_T1(5);
+            int nsw;
+            bool ok;
+#ifdef MQ_PROFILE_WAITS
+            const long long _t1 = clock64();
+#endif
+            const double sr = row_root_exact<G>(su, sx, a, b, lane, tw, s0, A, B, has, &nsw, &ok);
+#ifdef MQ_PROFILE_WAITS
+            if (wl == 0) atomicAdd(&g_wait_cycles[6], (unsigned long long)(clock64() - _t1));
+            const long long _t2 = clock64();
+#endif
+            if (has && b > a && lane == 0) {
+                my_sweeps += nsw;
+                if (!ok) ++my_faults;
+            }
+            const double inv_s = 1.0 / sr;
+            for (int t = a + lane; t < b; t += G) {
+                const double xn = fmax(sx[t] + tw * su[t] * inv_s, 0.0);
+                st.x[e0 + t] = xn;
+                __stcs(st.xbar + e0 + t, av.wold * sxb[t] + av.wnew * xn);
+            }
+#ifdef MQ_PROFILE_WAITS
+            if (wl == 0) atomicAdd(&g_wait_cycles[7], (unsigned long long)(clock64() - _t2));
+#endif
+        }
+        __syncwarp();
+        if (wl == 0) mbar_arrive(&empty[s]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        my_sweeps += __shfl_xor_sync(MQ_FULL, my_sweeps, o);
+        my_faults += __shfl_xor_sync(MQ_FULL, my_faults, o);
+    }
+    if (wl == 0 && my_sweeps)
+        atomicAdd((unsigned long long *)(st.pass_out + it), (unsigned long long)my_sweeps);
+    if (wl == 0 && my_faults)
+        atomicAdd((unsigned long long *)st.faults, (unsigned long long)my_faults);
 }
 
 // Long rows: one CTA per row; every sweep re-reads the row (L1/L2 resident).
@@ -207,16 +595,15 @@ __device__ __forceinline__ void block_sum3(double &a, double &b, double &c, doub
     c = group_sum<32>(rc);
 }
 
-__global__ void __launch_bounds__(kPrimalThreads)
-primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
-                   int64_t bin_lo, int64_t bin_hi) {
+__global__ void __launch_bounds__(256)
+primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
     __shared__ double sm[96];
     const double tau = st.steps[0];
     const Avg av = avg_weights(st.navg, it);
     int64_t my_sweeps = 0;
     int my_faults = 0;
-    for (int64_t r = bin_lo + blockIdx.x; r < bin_hi; r += gridDim.x) {
-        const int64_t i = mk.bin_rows[r];
+    for (int64_t r = blockIdx.x; r < mk.nlong; r += gridDim.x) {
+        const int64_t i = mk.long_rows[r];
         const int64_t a = mk.row_ptr[i], b = mk.row_ptr[i + 1];
         const double tw = tau * mk.w[i];
         double s0 = 0.0, A = 0.0, B = 0.0;
@@ -295,36 +682,34 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
 }
 
 // ------------------------------------------------------------ column sums
-// One warp per good, lanes stride the good's entries in transpose-schedule
-// order, four independent gathers in flight per lane, fixed butterfly tree.
+// Generic / long-row column sums over the blocked schedule: one thread per
+// good walking blocks [b_lo, b_hi) in order (ascending rows), 4 gathers in
+// flight.  acc_in (may be NULL) is the running sum to continue from.
 __global__ void __launch_bounds__(256)
-colsum_kernel(int64_t m, const int64_t *__restrict__ tptr, const int32_t *__restrict__ tperm,
-              const double *__restrict__ v, double *__restrict__ out, double *__restrict__ csbar,
-              const int64_t *__restrict__ navg, int it) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    Avg av = {0.0, 0.0};
-    if (csbar) av = avg_weights(navg, it);
-    for (int64_t j = warp_id; j < m; j += nwarps) {
-        const int64_t beg = tptr[j], end = tptr[j + 1];
-        double acc = 0.0;
-        int64_t t = beg + lane;
-        for (; t + 96 < end; t += 128) {
-            const int32_t k0 = __ldg(tperm + t), k1 = __ldg(tperm + t + 32);
-            const int32_t k2 = __ldg(tperm + t + 64), k3 = __ldg(tperm + t + 96);
-            const double v0 = v[k0], v1 = v[k1], v2 = v[k2], v3 = v[k3];
+colsum_blocks_kernel(int64_t m, const int32_t *__restrict__ bptr, const int32_t *__restrict__ bperm,
+                     int64_t b_lo, int64_t b_hi, const double *__restrict__ v,
+                     const double *__restrict__ acc_in, double *__restrict__ out,
+                     double *__restrict__ csbar, const int64_t *__restrict__ navg, int it) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    double acc = acc_in ? acc_in[j] : 0.0;
+    for (int64_t b = b_lo; b < b_hi; ++b) {
+        int64_t t = bptr[b * m + j];
+        const int64_t end = bptr[b * m + j + 1];
+        for (; t + 4 <= end; t += 4) {
+            const double v0 = v[bperm[t]], v1 = v[bperm[t + 1]];
+            const double v2 = v[bperm[t + 2]], v3 = v[bperm[t + 3]];
             acc += v0;
             acc += v1;
             acc += v2;
             acc += v3;
         }
-        for (; t < end; t += 32) acc += v[__ldg(tperm + t)];
-        acc = group_sum<32>(acc);
-        if (lane == 0) {
-            out[j] = acc;
-            if (csbar) csbar[j] = av.wold * csbar[j] + av.wnew * acc;
-        }
+        for (; t < end; ++t) acc += v[bperm[t]];
+    }
+    out[j] = acc;
+    if (csbar) {
+        const Avg av = avg_weights(navg, it);
+        csbar[j] = av.wold * csbar[j] + av.wnew * acc;
     }
 }
 
@@ -351,39 +736,59 @@ static int sm_count() {
     return n;
 }
 
-template <int G, int PER>
-static void launch_group(const mq_market &mk, const mq_state &st, int it, double *xprev,
-                         int64_t lo, int64_t hi, cudaStream_t s) {
-    const int64_t rows = hi - lo;
-    if (rows <= 0) return;
-    const int per_block = kPrimalThreads / G;
-    const int grid = grid_for(rows, per_block, sm_count() * 16);
-    primal_group_kernel<G, PER><<<grid, kPrimalThreads, 0, s>>>(mk, st, it, xprev, lo, hi);
-}
+#ifndef MQ_G
+#define MQ_G 16
+#endif
+#ifndef MQ_NCW
+#define MQ_NCW 6
+#endif
+#ifndef MQ_NSW
+#define MQ_NSW 16
+#endif
+constexpr int kG = MQ_G, kNSW = MQ_NSW, kNCW = MQ_NCW, kStages = 3;
+constexpr int kQMax = (1152 + kNCW * 32 - 1) / (kNCW * 32);
+using PrimalLayout = TileLayout<MQ_TILE_ENTRIES, MQ_TILE_ROWS>;
+static_assert(kQMax * kNCW * 32 >= kCsCols, "column-sum threads cannot cover a slice");
+constexpr int kPrimalSmem = kStages * PrimalLayout::kStage + 2 * kStages * 8 + 4 * kStages * 4 +
+                            (kCsCap + kCsCols + 8) * 4 + 4 * 8 + 16;
 
 int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev, cudaStream_t s) {
-    const int64_t *o = mk->bin_off;
-    launch_group<4, 1>(*mk, *st, it, xprev, o[0], o[1], s);    // len <= 4
-    launch_group<8, 1>(*mk, *st, it, xprev, o[1], o[2], s);    // <= 8
-    launch_group<16, 1>(*mk, *st, it, xprev, o[2], o[3], s);   // <= 16
-    launch_group<32, 1>(*mk, *st, it, xprev, o[3], o[4], s);   // <= 32
-    launch_group<32, 2>(*mk, *st, it, xprev, o[4], o[5], s);   // <= 64
-    launch_group<32, 4>(*mk, *st, it, xprev, o[5], o[6], s);   // <= 128
-    launch_group<32, 8>(*mk, *st, it, xprev, o[6], o[7], s);   // <= 256
-    launch_group<32, 16>(*mk, *st, it, xprev, o[7], o[8], s);  // <= 512
-    const int64_t nlong = o[9] - o[8];
-    if (nlong > 0) {
-        const int grid = grid_for(nlong, 1, sm_count() * 8);
-        primal_long_kernel<<<grid, kPrimalThreads, 0, s>>>(*mk, *st, it, xprev, o[8], o[9]);
+    static bool configured = false;
+    auto kern = primal_fused_kernel<kG, kNSW, kNCW, MQ_TILE_ENTRIES, MQ_TILE_ROWS, kStages, kQMax>;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kPrimalSmem);
+        if (e != cudaSuccess) return set_error(e, "mq_primal_step: smem attribute");
+        configured = true;
+    }
+    if (mk->ntiles > 0) {
+        if ((mk->m + mk->prim_grid - 1) / mk->prim_grid > (int64_t)kCsCols)
+            return set_error(cudaErrorInvalidValue, "mq_primal_step: too many goods per CTA");
+        cudaMemsetAsync(st->blk_done, 0, sizeof(int32_t) * 2 * (size_t)mk->nblk, s);
+        kern<<<mk->prim_grid, (kNSW + kNCW + 1) * 32, kPrimalSmem, s>>>(*mk, *st, it, xprev, 1);
+    } else {
+        cudaMemsetAsync(st->cs, 0, sizeof(double) * (size_t)mk->m, s);
+    }
+    if (mk->nlong > 0) {
+        const int grid = grid_for(mk->nlong, 1, sm_count() * 8);
+        primal_long_kernel<<<grid, 256, 0, s>>>(*mk, *st, it, xprev);
     }
     return check_launch("mq_primal_step");
 }
 
-int colsum_launch(const mq_market *mk, const double *v, double *out, double *csbar,
-                  const int64_t *navg, int it, cudaStream_t s) {
-    const int grid = grid_for(mk->m, 8, sm_count() * 32);
-    colsum_kernel<<<grid, 256, 0, s>>>(mk->m, mk->tptr, mk->tperm, v, out, csbar, navg, it);
-    return check_launch("colsum");
+// adds the long rows (pseudo-block nblk) to cs; csbar update when finalize
+int colsum_rest_launch(const mq_market *mk, const mq_state *st, int it, int finalize,
+                       cudaStream_t s) {
+    const int grid = (int)((mk->m + 255) / 256);
+    if (mk->nlong > 0) {
+        colsum_blocks_kernel<<<grid, 256, 0, s>>>(mk->m, mk->bptr, mk->bperm, mk->nblk,
+                                                  mk->nblk + 1, st->x, st->cs, st->cs,
+                                                  finalize ? st->csbar : nullptr, st->navg, it);
+    } else if (finalize) {
+        colsum_finalize_kernel<<<grid_for(mk->m, 256, sm_count() * 8), 256, 0, s>>>(
+            mk->m, st->cs, st->csbar, st->navg, it);
+    }
+    return check_launch("mq_colsum_step");
 }
 
 int dual_launch(const mq_market *mk, const mq_state *st, int it, cudaStream_t s) {
@@ -409,8 +814,7 @@ int mq_primal_step(const mq_market *mk, const mq_state *st, int it, double *x_pr
 }
 
 int mq_colsum_step(const mq_market *mk, const mq_state *st, int it, int finalize, void *stream) {
-    return colsum_launch(mk, st->x, st->cs, finalize ? st->csbar : nullptr, st->navg, it,
-                         (cudaStream_t)stream);
+    return colsum_rest_launch(mk, st, it, finalize, (cudaStream_t)stream);
 }
 
 int mq_colsum_finalize(const mq_market *mk, const mq_state *st, int it, void *stream) {
@@ -431,13 +835,26 @@ int mq_fast_chunk(const mq_market *mk, const mq_state *st, int iters, void *stre
     for (int it = 0; it < iters; ++it) {
         if ((rc = dual_launch(mk, st, it, s))) return rc;
         if ((rc = primal_launch(mk, st, it, nullptr, s))) return rc;
-        if ((rc = colsum_launch(mk, st->x, st->cs, st->csbar, st->navg, it, s))) return rc;
+        if ((rc = colsum_rest_launch(mk, st, it, 1, s))) return rc;
     }
     return mq_chunk_end(st, iters, stream);
 }
 
+// debug: read and reset the wait-cycle counters (zeros unless built with
+// -DMQ_PROFILE_WAITS); not part of the public header
+int mq_debug_counters(unsigned long long *out_host) {
+    cudaError_t e = cudaMemcpyFromSymbol(out_host, g_wait_cycles, sizeof(g_wait_cycles));
+    if (e != cudaSuccess) return set_error(e, "mq_debug_counters");
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    e = cudaMemcpyToSymbol(g_wait_cycles, z, sizeof(z));
+    return e == cudaSuccess ? 0 : set_error(e, "mq_debug_counters");
+}
+
 int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream) {
-    return colsum_launch(mk, v, out, nullptr, nullptr, 0, (cudaStream_t)stream);
+    const int grid = (int)((mk->m + 255) / 256);
+    colsum_blocks_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+        mk->m, mk->bptr, mk->bperm, 0, mk->nblk + 1, v, nullptr, out, nullptr, nullptr, 0);
+    return check_launch("mq_colsum");
 }
 
 }  // extern "C"

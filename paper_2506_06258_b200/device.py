@@ -1,39 +1,146 @@
 """Device-resident market: the HBM layout of DESIGN.md §3, owned by torch.
 
-    row_ptr  int64 [n+1]    col    int32 [nnz]   u  float64 [nnz] (row max 1)
-    u_orig   float64 [nnz]  w      float64 [n]   scales float64 [n]
-    tptr     int64 [m+1]    tperm  int32 [nnz]   (stable column grouping)
-    bin_rows int32 [n]      rows grouped by length bin for the primal kernels
+    row_ptr  int64 [n+1 (+pad)]   w       float64 [n (+pad)]   scales float64 [n]
+    col      int32 [nnz (+pad)]   u       float64 [nnz (+pad)] (row max 1)
+    u_orig   float64 [nnz]        (residuals are measured on the original data)
+    tiles    int64 [ntiles, 2]    row ranges of <= 2048 entries / 256 rows
+    long_rows int32 [nlong]       rows longer than 1024 entries
+    bperm    int32 [nnz]          tile-blocked transpose schedule: per block of
+    bptr     int32 [(nblk+1)m+1]  8 x prim_grid tiles, per good, ascending rows
+                                  (pseudo-block nblk = the long rows)
+    tperm / tptr                  the reference's global schedule (sparse.py:
+                                  130-145), only for the k-section drop-in
+(pad) = 16 readable elements past the end for the TMA bulk copies.
 
-Built once per instance (or per shard); every later call only passes the
+Built once per instance (or per row shard); every later call only passes the
 `mq_market` struct of raw pointers to the native library.
 """
+
+import ctypes
+import warnings
 
 import numpy as np
 import torch
 
 from . import _native as nat
 
-# upper row length of bins 0..7 of the primal kernel (bin 8 = longer rows)
-BIN_EDGES = (4, 8, 16, 32, 64, 128, 256, 512)
-
 
 def _stream():
-    return ctypes_stream(torch.cuda.current_stream())
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def ctypes_stream(s):
-    import ctypes
+def _padded(src, dtype, device):
+    """Copy of `src` with nat.PAD extra (zero) elements; returns (buffer, view)."""
+    n = int(src.numel()) if isinstance(src, torch.Tensor) else len(src)
+    buf = torch.zeros(n + nat.PAD, dtype=dtype, device=device)
+    if n:
+        if isinstance(src, torch.Tensor):
+            buf[:n].copy_(src)
+        else:
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                buf[:n].copy_(torch.from_numpy(np.ascontiguousarray(src)))
+    return buf, buf[:n]
 
-    return ctypes.c_void_p(s.cuda_stream)
+
+def build_tiles(row_ptr, tile_entries=nat.TILE_ENTRIES, long_row=nat.LONG_ROW,
+                tile_rows=nat.TILE_ROWS):
+    """Contiguous runs of rows with <= tile_entries entries and <= tile_rows
+    rows; rows longer than long_row go to a separate list.
+    Returns (tiles [k,2] int64, long int32)."""
+    dev = row_ptr.device
+    n = row_ptr.numel() - 1
+    lens = row_ptr[1:] - row_ptr[:-1]
+    is_long = lens > long_row
+    long_rows = torch.nonzero(is_long).flatten().to(torch.int32)
+    short = ~is_long
+    if int(short.sum().item()) == 0:
+        return torch.zeros(0, 2, dtype=torch.int64, device=dev), long_rows
+    max_short = int(lens[short].max().item())
+    span = max(1, tile_entries - max_short)
+    # segment = run of short rows between long rows; its base is the end of
+    # the previous long row
+    seg = torch.cumsum(is_long.to(torch.int64), 0)
+    ends = torch.where(is_long, row_ptr[1:], torch.zeros_like(lens))
+    base = torch.cummax(ends, 0).values
+    nnz = int(row_ptr[-1].item())
+    # first row of each segment, for the row-count window
+    starts_row = torch.where(is_long, torch.arange(1, n + 1, device=dev),
+                             torch.zeros_like(lens))
+    seg_row0 = torch.cummax(starts_row, 0).values
+    rows_all = torch.arange(n, device=dev)
+    ewin = (row_ptr[:-1] - base) // span
+    rwin = (rows_all - seg_row0) // tile_rows
+    key = (seg * (nnz // span + 2) + ewin) * (n // tile_rows + 2) + rwin
+    rows = torch.arange(n, device=dev)[short]
+    k = key[short]
+    change = torch.ones_like(k, dtype=torch.bool)
+    change[1:] = k[1:] != k[:-1]
+    starts = torch.nonzero(change).flatten()
+    last = torch.cat([starts[1:] - 1, torch.tensor([rows.numel() - 1], device=dev)])
+    tiles = torch.stack([rows[starts], rows[last] + 1], 1).contiguous()
+    return tiles, long_rows
+
+
+TILES_PER_CTA_PER_BLOCK = 4
+
+
+def sm_count(device):
+    return torch.cuda.get_device_properties(device).multi_processor_count
+
+
+def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
+                           tiles_per_cta=TILES_PER_CTA_PER_BLOCK):
+    """Entry positions grouped by (block of tiles, good), ascending inside a
+    good; long-row entries form the last pseudo-block.  Returns
+    (bperm int32 [nnz], bptr int32 [(nblk+1)*m+1], nblk, tiles_per_block)."""
+    dev = col.device
+    nnz = col.numel()
+    ntiles = int(tiles.shape[0])
+    tpb = max(1, tiles_per_cta * max(1, prim_grid))
+    nblk = -(-ntiles // tpb)
+    pos = torch.arange(nnz, device=dev, dtype=torch.int64)
+    if nblk:
+        starts = row_ptr[tiles[::tpb, 0]].contiguous()
+        blk = torch.searchsorted(starts, pos, right=True) - 1
+    else:
+        blk = torch.zeros(nnz, dtype=torch.int64, device=dev)
+    del pos
+    if long_rows.numel():
+        lr = long_rows.to(torch.int64)
+        d = torch.zeros(nnz + 1, dtype=torch.int32, device=dev)
+        d.index_add_(0, row_ptr[lr], torch.ones_like(lr, dtype=torch.int32))
+        d.index_add_(0, row_ptr[lr + 1], -torch.ones_like(lr, dtype=torch.int32))
+        is_long = torch.cumsum(d, 0, dtype=torch.int32)[:nnz] > 0
+        del d
+        blk = torch.where(is_long, torch.full_like(blk, nblk), blk)
+        del is_long
+    total = (nblk + 1) * m
+    if total < 2 ** 31:
+        key = blk.to(torch.int32) * m + col
+    else:
+        key = blk * m + col.to(torch.int64)
+    del blk
+    _, perm = torch.sort(key, stable=True)
+    # [pad]: the fused kernel stages slices of both arrays with TMA bulk copies
+    bperm = torch.zeros(nnz + nat.PAD, dtype=torch.int32, device=dev)
+    bperm[:nnz] = perm
+    del perm
+    counts = torch.bincount(key.to(torch.int64), minlength=total)
+    del key
+    bptr = torch.zeros(total + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(counts, 0, out=bptr[1:])
+    bptr32 = torch.zeros(total + 1 + nat.PAD, dtype=torch.int32, device=dev)
+    bptr32[:total + 1] = bptr
+    return bperm[:nnz], bptr32[:total + 1], nblk, tpb
 
 
 class DeviceMarket:
     """CSR utilities + budgets on one GPU (optionally a row shard).
 
-    Parameters are host numpy arrays or device tensors: row_ptr (n+1),
-    col (nnz), u_orig (nnz, original utilities), w (n).  m is the number of
-    goods (global).  row_begin is the global index of the first row.
+    row_ptr (n+1), col (nnz), u_orig (nnz, original utilities), w (n) are host
+    numpy arrays or device tensors; m is the (global) number of goods;
+    row_begin the global index of the first row.
     """
 
     def __init__(self, row_ptr, col, u_orig, w, m, device=None, row_begin=0, lib=None):
@@ -46,49 +153,53 @@ class DeviceMarket:
         def up(a, dtype):
             if isinstance(a, torch.Tensor):
                 return a.to(device=dev, dtype=dtype).contiguous()
-            return torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dtype)
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                return torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dtype)
 
         with torch.cuda.device(dev):
-            self.row_ptr = up(row_ptr, torch.int64)
-            self.col = up(col, torch.int32)
-            self.u_orig = up(u_orig, torch.float64)
-            self.w = up(w, torch.float64)
+            self._rp_buf, self.row_ptr = _padded(up(row_ptr, torch.int64), torch.int64, dev)
             self.n = int(self.row_ptr.numel() - 1)
             self.m = int(m)
+            self._col_buf, self.col = _padded(up(col, torch.int32), torch.int32, dev)
             self.nnz = int(self.col.numel())
+            self.u_orig = up(u_orig, torch.float64)
+            self._w_buf, self.w = _padded(up(w, torch.float64), torch.float64, dev)
             self.row_begin = int(row_begin)
             if int(self.row_ptr[-1].item()) != self.nnz:
                 raise ValueError("row_ptr[-1] does not match nnz")
+            if self.nnz >= 2 ** 31:
+                raise ValueError("a shard must hold < 2^31 entries (int32 positions)")
             # normalization on device (instance.py:118-138, same IEEE division)
-            self.u = torch.empty_like(self.u_orig)
+            self._u_buf = torch.zeros(self.nnz + nat.PAD, dtype=torch.float64, device=dev)
+            self.u = self._u_buf[:self.nnz]
             self.scales = torch.empty(self.n, dtype=torch.float64, device=dev)
-            nat.check(self.lib.mq_normalize_rows(self.n, nat.ptr(self.row_ptr), nat.ptr(self.u_orig),
-                                                 nat.ptr(self.u), nat.ptr(self.scales), _stream()),
+            nat.check(self.lib.mq_normalize_rows(self.n, nat.ptr(self.row_ptr),
+                                                 nat.ptr(self.u_orig), nat.ptr(self.u),
+                                                 nat.ptr(self.scales), _stream()),
                       "mq_normalize_rows")
-            # transpose schedule: stable sort of columns = ascending row inside
-            # every column (sparse.py:130-145)
-            if self.nnz:
+            self.col_counts = (torch.bincount(self.col.to(torch.int64), minlength=self.m)
+                               if self.nnz else torch.zeros(self.m, dtype=torch.int64,
+                                                            device=dev))
+            self.tiles, self.long_rows = build_tiles(self.row_ptr)
+            self.prim_grid = int(min(max(1, self.tiles.shape[0]), sm_count(dev)))
+            self.bperm, self.bptr, self.nblk, self.tiles_per_block = build_blocked_schedule(
+                self.row_ptr, self.col, self.m, self.tiles, self.long_rows, self.prim_grid)
+            lens = self.row_ptr[1:] - self.row_ptr[:-1]
+            self.max_row_len = int(lens.max().item()) if self.n else 0
+        self.tperm = self.tptr = None
+        self.struct = self._make_struct()
+
+    def global_schedule(self):
+        """(tperm int32, tptr int64): the reference's transpose schedule, for
+        the k-section drop-in (built on first use)."""
+        if self.tperm is None:
+            with torch.cuda.device(self.device):
                 _, perm = torch.sort(self.col, stable=True)
                 self.tperm = perm.to(torch.int32)
-                del perm
-                counts = torch.bincount(self.col.to(torch.int64), minlength=self.m)
-            else:
-                self.tperm = torch.zeros(0, dtype=torch.int32, device=dev)
-                counts = torch.zeros(self.m, dtype=torch.int64, device=dev)
-            self.col_counts = counts
-            self.tptr = torch.zeros(self.m + 1, dtype=torch.int64, device=dev)
-            torch.cumsum(counts, 0, out=self.tptr[1:])
-            # row-length bins for the primal kernels
-            lens = self.row_ptr[1:] - self.row_ptr[:-1]
-            edges = torch.tensor(BIN_EDGES, dtype=torch.int64, device=dev)
-            bins = torch.bucketize(lens, edges, right=False)
-            order = torch.sort(bins, stable=True)[1]
-            self.bin_rows = order.to(torch.int32)
-            bc = torch.bincount(bins, minlength=len(BIN_EDGES) + 1).cpu().numpy()
-            self.bin_off = np.zeros(len(BIN_EDGES) + 2, dtype=np.int64)
-            self.bin_off[1:] = np.cumsum(bc)
-            self.max_row_len = int(lens.max().item()) if self.n else 0
-        self.struct = self._make_struct()
+                self.tptr = torch.zeros(self.m + 1, dtype=torch.int64, device=self.device)
+                torch.cumsum(self.col_counts, 0, out=self.tptr[1:])
+        return self.tperm, self.tptr
 
     def _make_struct(self):
         s = nat.MqMarket()
@@ -98,11 +209,15 @@ class DeviceMarket:
         s.u = self.u.data_ptr()
         s.u_orig = self.u_orig.data_ptr()
         s.w = self.w.data_ptr()
-        s.tptr = self.tptr.data_ptr()
-        s.tperm = self.tperm.data_ptr()
-        s.bin_rows = self.bin_rows.data_ptr()
-        for k in range(nat.NBINS + 1):
-            s.bin_off[k] = int(self.bin_off[k])
+        s.tiles = self.tiles.data_ptr()
+        s.ntiles = int(self.tiles.shape[0])
+        s.long_rows = self.long_rows.data_ptr()
+        s.nlong = int(self.long_rows.numel())
+        s.bperm = self.bperm.data_ptr()
+        s.bptr = self.bptr.data_ptr()
+        s.nblk = int(self.nblk)
+        s.tiles_per_block = int(self.tiles_per_block)
+        s.prim_grid = int(self.prim_grid)
         s.row_begin = self.row_begin
         return s
 
@@ -114,10 +229,13 @@ class DeviceMarket:
 
     def set_budgets(self, w):
         """Replace budgets in place (Arrow-Debreu outer loop)."""
-        self.w.copy_(torch.as_tensor(np.asarray(w, dtype=np.float64)) if not isinstance(
-            w, torch.Tensor) else w)
+        if not isinstance(w, torch.Tensor):
+            w = torch.as_tensor(np.asarray(w, dtype=np.float64))
+        self.w.copy_(w)
 
     def bytes_resident(self):
-        ts = (self.row_ptr, self.col, self.u, self.u_orig, self.w, self.scales, self.tptr,
-              self.tperm, self.bin_rows)
+        ts = [self._rp_buf, self._col_buf, self._u_buf, self.u_orig, self._w_buf, self.scales,
+              self.tiles, self.long_rows, self.bperm, self.bptr]
+        if self.tperm is not None:
+            ts += [self.tperm, self.tptr]
         return sum(t.numel() * t.element_size() for t in ts)

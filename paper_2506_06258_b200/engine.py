@@ -56,9 +56,14 @@ class PdhcgEngine:
         dev = dm.device
         f64 = dict(dtype=torch.float64, device=dev)
         nnz, m = dm.nnz, dm.m
-        self.x = torch.zeros(nnz, **f64)
-        self.xbar = torch.zeros(nnz, **f64)
+        # x / xbar are read by TMA bulk copies: nat.PAD readable elements past nnz
+        self._x_buf = torch.zeros(nnz + nat.PAD, **f64)
+        self._xbar_buf = torch.zeros(nnz + nat.PAD, **f64)
+        self.x = self._x_buf[:nnz]
+        self.xbar = self._xbar_buf[:nnz]
         self.x0 = torch.zeros(nnz, **f64)
+        # per block: tiles solved, then column-sum warps done (throttle)
+        self.blk_done = torch.zeros(max(1, 2 * dm.nblk), dtype=torch.int32, device=dev)
         self.p = torch.zeros(m, **f64)
         self.pbar = torch.zeros(m, **f64)
         self.p0 = torch.zeros(m, **f64)
@@ -86,7 +91,8 @@ class PdhcgEngine:
     # ------------------------------------------------------------ plumbing
     def _make_state(self):
         s = nat.MqState()
-        for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "steps", "faults"):
+        for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "blk_done", "steps",
+                     "faults"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.navg = self.navg_dev.data_ptr()
         s.pass_out = self.pass_buf.data_ptr()
@@ -235,11 +241,12 @@ class PdhcgEngine:
         import ctypes
 
         dm = self.dm
+        tperm, tptr = dm.global_schedule()
         navg_out = ctypes.c_int64(0)
         self.set_steps(self.tau, self.sigma)
         rc = self.lib.mq_pdhcg_chunk(
-            dm.n, dm.m, nat.ptr(dm.row_ptr), nat.ptr(dm.col), nat.ptr(dm.u), nat.ptr(dm.tperm),
-            nat.ptr(dm.tptr), nat.ptr(dm.w), nat.ptr(self.x), nat.ptr(self.x_prev),
+            dm.n, dm.m, nat.ptr(dm.row_ptr), nat.ptr(dm.col), nat.ptr(dm.u), nat.ptr(tperm),
+            nat.ptr(tptr), nat.ptr(dm.w), nat.ptr(self.x), nat.ptr(self.x_prev),
             nat.ptr(self.p), nat.ptr(self.xbar), nat.ptr(self.pbar), self.navg, self.tau,
             self.sigma, self.sections, self.subtol, iters, nat.ptr(self.c_buf),
             nat.ptr(self.pass_buf), ctypes.byref(navg_out), _cur_stream())

@@ -180,3 +180,73 @@ def test_abi_marshaling_without_device():
         rc = getattr(lib, name)(*args)
         assert rc != 0, name
         assert lib.mq_last_error()
+
+
+def _random_csr(rng, n, m, lens):
+    rows = [np.sort(rng.choice(m, size=min(int(l), m), replace=False)) for l in lens]
+    rp = np.zeros(n + 1, dtype=np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    col = np.concatenate(rows) if rows else np.zeros(0, dtype=np.int64)
+    return rp, col
+
+
+def test_primal_tiles_cover_rows_once():
+    """Tiles are contiguous runs of short rows with <= 2048 entries; long
+    rows are listed separately; every row appears exactly once."""
+    import torch
+
+    from paper_2506_06258_b200.device import build_tiles
+
+    rng = np.random.default_rng(0)
+    for lens in (rng.poisson(100, 3000), np.minimum(1 + rng.pareto(1.1, 3000) * 20, 5000),
+                 np.full(40, 700), np.array([0, 3, 2000, 0, 5, 1500, 7]),
+                 np.ones(5000, dtype=np.int64), rng.integers(1, 4, 3000)):
+        lens = np.asarray(lens, dtype=np.int64)
+        rp = np.zeros(len(lens) + 1, dtype=np.int64)
+        rp[1:] = np.cumsum(lens)
+        tiles, long_rows = build_tiles(torch.from_numpy(rp), 2048, 1024)
+        tiles = tiles.numpy()
+        seen = np.zeros(len(lens), dtype=int)
+        for r0, r1 in tiles:
+            assert r1 > r0
+            assert rp[r1] - rp[r0] <= 2048 and r1 - r0 <= 256
+            assert np.all(lens[r0:r1] <= 1024)
+            seen[r0:r1] += 1
+        seen[long_rows.numpy()] += 1
+        assert np.all(seen == 1)
+        assert set(long_rows.tolist()) == set(np.flatnonzero(lens > 1024).tolist())
+
+
+def test_blocked_schedule_preserves_column_order():
+    """Walking a good block by block (tiles, then the long-row pseudo-block)
+    visits its tile entries in ascending row order, and every entry once."""
+    import torch
+
+    from paper_2506_06258_b200.device import build_blocked_schedule, build_tiles
+
+    rng = np.random.default_rng(1)
+    n, m = 700, 60
+    lens = rng.poisson(8, n) + 1
+    lens[[5, 300, 301, 650]] = [59, 45, 50, 40]     # long rows (threshold 30 below)
+    rp, col = _random_csr(rng, n, m, lens)
+    rpt = torch.from_numpy(rp)
+    tiles, long_rows = build_tiles(rpt, 64, 30, 16)
+    bperm, bptr, nblk, tpb = build_blocked_schedule(rpt, torch.from_numpy(col.astype(np.int32)),
+                                                    m, tiles, long_rows, prim_grid=3,
+                                                    tiles_per_cta=2)
+    bperm, bptr = bperm.numpy(), bptr.numpy()
+    assert tpb == 6 and nblk == -(-tiles.shape[0] // 6)
+    assert np.array_equal(np.sort(bperm), np.arange(len(col)))
+    row_of = np.repeat(np.arange(n), np.diff(rp))
+    is_long = np.isin(row_of, long_rows.numpy())
+    tstart = rp[tiles[:, 0].numpy()]
+    for j in range(m):
+        walk = np.concatenate([bperm[bptr[b * m + j]:bptr[b * m + j + 1]] for b in range(nblk)])
+        ref = np.flatnonzero((col == j) & ~is_long)
+        assert np.array_equal(walk, ref)
+        lw = bperm[bptr[nblk * m + j]:bptr[nblk * m + j + 1]]
+        assert np.array_equal(lw, np.flatnonzero((col == j) & is_long))
+        for b in range(nblk):
+            seg = bperm[bptr[b * m + j]:bptr[b * m + j + 1]]
+            blk = np.searchsorted(tstart[::6], seg, side="right") - 1
+            assert np.all(blk == b)

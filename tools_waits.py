@@ -1,0 +1,37 @@
+"""Debug: wait-cycle breakdown of the fused primal kernel (build with
+python -m paper_2506_06258_b200._build --profile-waits)."""
+import ctypes
+import sys
+
+import numpy as np
+import torch
+
+sys.argv += ["--no-cpu", "--no-e2e"]
+import bench
+from paper_2506_06258_b200 import _native as nat
+
+cfg = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "c4"
+shard = bench.shard_rows(cfg, 0, 1, 0)
+dm, eng = bench.make_session(shard, None)
+lib = nat.load_library()
+lib.mq_debug_counters.argtypes = [ctypes.c_void_p]
+buf = (ctypes.c_ulonglong * 8)()
+bench.run_iters(eng, 3)
+torch.cuda.synchronize()
+lib.mq_debug_counters(buf)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+bench.run_iters(eng, 10)
+e1.record()
+torch.cuda.synchronize()
+lib.mq_debug_counters(buf)
+ms = e0.elapsed_time(e1) / 10
+cyc = ms * 1e-3 * 1.965e9
+nsm = dm.prim_grid
+names = ["solver wait tile", "solver throttled", "producer wait stage", "colsum wait block",
+         "colsum gather", "solver pass1", "solver root", "solver write"]
+print(f"{cfg}: {ms:.3f} ms/iter, kernel-cycles/SM ~{cyc:.3e}")
+per_warp = {0: 16, 1: 16, 2: 1, 3: 1, 4: 1, 5: 16, 6: 16, 7: 16}
+for i, nm in enumerate(names):
+    v = buf[i] / 10 / nsm / per_warp[i]
+    print(f"  {nm:22s} {v:.3e} cycles per warp per iter ({100 * v / cyc:.1f}% of iter)")
