@@ -183,7 +183,7 @@ def kernel_breakdown(eng, iters):
 
     from paper_2506_06258_b200 import _native as nat
 
-    lib, mk, st = eng.lib, eng.dm.struct, eng.state
+    lib, mk, st = eng.ops.lib, eng.dm.struct, eng.state
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(iters)]
     eng.pass_buf.zero_()
     eng.faults.zero_()

@@ -34,13 +34,79 @@ def _cur_stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+class NativeOps:
+    """The engine's device operations, each one call into libmarket_eq_b200.so
+    on the current CUDA stream (include/market_eq_b200.h)."""
+
+    supports_graphs = True
+
+    def __init__(self, dm, engine):
+        self.lib, self.dm, self.eng = dm.lib, dm, engine
+
+    def _c(self, rc, what):
+        return nat.check(rc, what)
+
+    def colsum(self, v, out):
+        self._c(self.lib.mq_colsum(self.dm.struct, nat.ptr(v), nat.ptr(out), _cur_stream()),
+                "mq_colsum")
+
+    def dual(self, it):
+        self._c(self.lib.mq_dual_step(self.dm.struct, self.eng.state, it, _cur_stream()),
+                "mq_dual_step")
+
+    def primal(self, it):
+        self._c(self.lib.mq_primal_step(self.dm.struct, self.eng.state, it, None, _cur_stream()),
+                "mq_primal_step")
+
+    def colsum_rest(self, it, finalize):
+        self._c(self.lib.mq_colsum_step(self.dm.struct, self.eng.state, it, int(finalize),
+                                        _cur_stream()), "mq_colsum_step")
+
+    def finalize(self, it):
+        self._c(self.lib.mq_colsum_finalize(self.dm.struct, self.eng.state, it, _cur_stream()),
+                "mq_colsum_finalize")
+
+    def chunk_end(self, iters):
+        self._c(self.lib.mq_chunk_end(self.eng.state, iters, _cur_stream()), "mq_chunk_end")
+
+    def resid_rows(self, x, p, use_norm, colbest, t_out, out, scratch):
+        self._c(self.lib.mq_resid_rows(self.dm.struct, nat.ptr(x), nat.ptr(p), int(use_norm),
+                                       nat.ptr(colbest), nat.ptr(t_out), None, nat.ptr(out),
+                                       nat.ptr(scratch), _cur_stream()), "mq_resid_rows")
+
+    def resid_cols(self, cs, p, colbest, out, scratch):
+        self._c(self.lib.mq_resid_cols(self.dm.m, nat.ptr(cs), nat.ptr(p), nat.ptr(colbest),
+                                       nat.ptr(out), nat.ptr(scratch), _cur_stream()),
+                "mq_resid_cols")
+
+    def restart_moves(self, xbar, x0, pbar, p0, csbar, cs0, out, scratch):
+        self._c(self.lib.mq_restart_moves(self.dm.struct, nat.ptr(xbar), nat.ptr(x0),
+                                          nat.ptr(pbar), nat.ptr(p0), nat.ptr(csbar),
+                                          nat.ptr(cs0), nat.ptr(out), nat.ptr(scratch),
+                                          _cur_stream()), "mq_restart_moves")
+
+    def ksection_chunk(self, iters):
+        """mq_pdhcg_chunk on the engine's buffers -> (faults, navg)."""
+        import ctypes
+
+        e, dm = self.eng, self.dm
+        tperm, tptr = dm.global_schedule()
+        navg_out = ctypes.c_int64(0)
+        rc = self.lib.mq_pdhcg_chunk(
+            dm.n, dm.m, nat.ptr(dm.row_ptr), nat.ptr(dm.col), nat.ptr(dm.u), nat.ptr(tperm),
+            nat.ptr(tptr), nat.ptr(dm.w), nat.ptr(e.x), nat.ptr(e.x_prev), nat.ptr(e.p),
+            nat.ptr(e.xbar), nat.ptr(e.pbar), e.navg, e.tau, e.sigma, e.sections, e.subtol,
+            iters, nat.ptr(e.c_buf), nat.ptr(e.pass_buf), ctypes.byref(navg_out), _cur_stream())
+        self._c(rc, "mq_pdhcg_chunk")
+        return rc, int(navg_out.value)
+
+
 class PdhcgEngine:
     def __init__(self, dm, row_solver="exact", sections=32, subproblem_tol=1e-10,
-                 use_graphs=True, group=None):
+                 use_graphs=True, group=None, ops_factory=None):
         if row_solver not in ("exact", "ksection"):
             raise ValueError("row_solver must be 'exact' or 'ksection'")
         self.dm = dm
-        self.lib = dm.lib
         self.mode = row_solver
         self.sections = int(sections)
         self.subtol = float(subproblem_tol)
@@ -52,7 +118,9 @@ class PdhcgEngine:
             self.world = dist.get_world_size(group)
         if self.mode == "ksection" and self.world > 1:
             raise ValueError("the k-section drop-in runs on a single GPU")
-        self.use_graphs = bool(use_graphs) and self.world == 1
+        self.ops = (ops_factory or NativeOps)(dm, self)
+        self.use_graphs = (bool(use_graphs) and self.world == 1
+                           and getattr(self.ops, "supports_graphs", False))
         dev = dm.device
         f64 = dict(dtype=torch.float64, device=dev)
         nnz, m = dm.nnz, dm.m
@@ -76,8 +144,9 @@ class PdhcgEngine:
         self.navg_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         self.faults = torch.zeros(1, dtype=torch.int64, device=dev)
         self.pass_buf = torch.zeros(1024, dtype=torch.int64, device=dev)
-        self.scratch = torch.zeros(int(self.lib.mq_scratch_doubles()), **f64)
-        self.scratch2 = torch.zeros(int(self.lib.mq_scratch_doubles()), **f64)
+        nscr = int(dm.lib.mq_scratch_doubles()) if hasattr(dm, "lib") else 16
+        self.scratch = torch.zeros(nscr, **f64)
+        self.scratch2 = torch.zeros(nscr, **f64)
         self.out = torch.zeros(32, **f64)
         self.t_buf = torch.zeros(dm.n, **f64)
         if self.mode == "ksection":
@@ -90,6 +159,8 @@ class PdhcgEngine:
 
     # ------------------------------------------------------------ plumbing
     def _make_state(self):
+        if not isinstance(self.ops, NativeOps):
+            return None
         s = nat.MqState()
         for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "blk_done", "steps",
                      "faults"):
@@ -108,8 +179,7 @@ class PdhcgEngine:
         return t
 
     def colsum(self, v, out):
-        nat.check(self.lib.mq_colsum(self.dm.struct, nat.ptr(v), nat.ptr(out), _cur_stream()),
-                  "mq_colsum")
+        self.ops.colsum(v, out)
         return self._allreduce(out)
 
     # ------------------------------------------------------------ state
@@ -208,22 +278,24 @@ class PdhcgEngine:
         return [int(v) for v in vals[:-1]]
 
     def _launch_chunk(self, iters):
-        lib, mk, st = self.lib, self.dm.struct, self.state
+        """One chunk: per iteration price step, fused prox + column sums, and on
+        N ranks the all-reduce of the m-length column sums before the running
+        average of colsum(xbar) is updated."""
+        ops = self.ops
         self.pass_buf[:iters].zero_()
         self.faults.zero_()
-        fin = 1 if self.world == 1 else 0
+        single = self.world == 1
         for it in range(iters):
-            s = _cur_stream()
-            nat.check(lib.mq_dual_step(mk, st, it, s), "mq_dual_step")
-            nat.check(lib.mq_primal_step(mk, st, it, None, s), "mq_primal_step")
-            nat.check(lib.mq_colsum_step(mk, st, it, fin, s), "mq_colsum_step")
-            if not fin:
+            ops.dual(it)
+            ops.primal(it)
+            ops.colsum_rest(it, single)
+            if not single:
                 self._allreduce(self.cs)
-                nat.check(lib.mq_colsum_finalize(mk, st, it, s), "mq_colsum_finalize")
-        if self.world > 1:
+                ops.finalize(it)
+        if not single:
             self._allreduce(self.pass_buf[:iters])
             self._allreduce(self.faults)
-        nat.check(lib.mq_chunk_end(st, iters, _cur_stream()), "mq_chunk_end")
+        ops.chunk_end(iters)
 
     def _capture(self, iters):
         g = torch.cuda.CUDAGraph()
@@ -238,22 +310,10 @@ class PdhcgEngine:
         return g
 
     def _run_chunk_ksection(self, iters):
-        import ctypes
-
-        dm = self.dm
-        tperm, tptr = dm.global_schedule()
-        navg_out = ctypes.c_int64(0)
-        self.set_steps(self.tau, self.sigma)
-        rc = self.lib.mq_pdhcg_chunk(
-            dm.n, dm.m, nat.ptr(dm.row_ptr), nat.ptr(dm.col), nat.ptr(dm.u), nat.ptr(tperm),
-            nat.ptr(tptr), nat.ptr(dm.w), nat.ptr(self.x), nat.ptr(self.x_prev),
-            nat.ptr(self.p), nat.ptr(self.xbar), nat.ptr(self.pbar), self.navg, self.tau,
-            self.sigma, self.sections, self.subtol, iters, nat.ptr(self.c_buf),
-            nat.ptr(self.pass_buf), ctypes.byref(navg_out), _cur_stream())
-        nat.check(rc, "mq_pdhcg_chunk")
+        rc, navg = self.ops.ksection_chunk(iters)
         if rc > 0:
             raise SubproblemError(f"{rc} row subproblems exceeded {MAX_ROW_PASSES} passes")
-        self.navg = int(navg_out.value)
+        self.navg = navg
         self.navg_dev.fill_(self.navg)
         # column sums of the iterates for residuals / restart moves
         self.colsum(self.x, self.cs)
@@ -264,11 +324,8 @@ class PdhcgEngine:
     # ------------------------------------------------------------ reductions
     def _rows(self, x, p, use_norm, k, t_out=None):
         self.colbest[k].zero_()
-        nat.check(self.lib.mq_resid_rows(self.dm.struct, nat.ptr(x), nat.ptr(p), int(use_norm),
-                                         nat.ptr(self.colbest[k]), nat.ptr(t_out), None,
-                                         nat.ptr(self.out[16 * k: 16 * k + 8]),
-                                         nat.ptr(self.scratch if k == 0 else self.scratch2),
-                                         _cur_stream()), "mq_resid_rows")
+        self.ops.resid_rows(x, p, use_norm, self.colbest[k], t_out, self.out[16 * k: 16 * k + 8],
+                            self.scratch if k == 0 else self.scratch2)
         if self.world > 1:
             o = self.out[16 * k: 16 * k + 8]
             self._allreduce(self.colbest[k], "max")
@@ -283,11 +340,8 @@ class PdhcgEngine:
             o[5:7].copy_(sm)
 
     def _cols(self, cs, p, k):
-        nat.check(self.lib.mq_resid_cols(self.dm.m, nat.ptr(cs), nat.ptr(p),
-                                         nat.ptr(self.colbest[k]),
-                                         nat.ptr(self.out[16 * k + 8: 16 * k + 14]),
-                                         nat.ptr(self.scratch if k == 0 else self.scratch2),
-                                         _cur_stream()), "mq_resid_cols")
+        self.ops.resid_cols(cs, p, self.colbest[k], self.out[16 * k + 8: 16 * k + 14],
+                            self.scratch if k == 0 else self.scratch2)
 
     @staticmethod
     def _assemble(v):
@@ -330,11 +384,8 @@ class PdhcgEngine:
         """(||dx||, ||dp||, ||dx||^2, ||dp||^2, |colsum(dx).dp|) of the average
         against the last restart point (driver.py:156-162)."""
         o = self.out[24:28]
-        nat.check(self.lib.mq_restart_moves(self.dm.struct, nat.ptr(self.xbar), nat.ptr(self.x0),
-                                            nat.ptr(self.pbar), nat.ptr(self.p0),
-                                            nat.ptr(self.csbar), nat.ptr(self.cs0), nat.ptr(o),
-                                            nat.ptr(self.scratch), _cur_stream()),
-                  "mq_restart_moves")
+        self.ops.restart_moves(self.xbar, self.x0, self.pbar, self.p0, self.csbar, self.cs0, o,
+                               self.scratch)
         if self.world > 1:
             sx = o[0:1].clone()
             self._allreduce(sx, "sum")

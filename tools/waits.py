@@ -7,6 +7,7 @@ import numpy as np
 import torch
 
 sys.argv += ["--no-cpu", "--no-e2e"]
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import bench
 from paper_2506_06258_b200 import _native as nat
 
