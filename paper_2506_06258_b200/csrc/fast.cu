@@ -340,6 +340,9 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         return;
     }
 
+#ifdef MQ_NO_COLSUM  // timing experiment only: solver without column sums
+    if (warp > NSW) return;
+#endif
     if (warp > NSW) {  // ---------------------------------------- column sums
         // The CTA's NCW column-sum warps own goods [j_lo, j_hi); thread ct owns
         // j_lo + ct + q*NCW*32.  Per block, one thread stages the block's
@@ -479,9 +482,11 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         const int64_t blk = k / tpb_all;
         {
             MQ_T0();
+#ifndef MQ_NO_COLSUM
             if (blk >= kLag && wl == 0)
                 wait_counter(st.blk_done + mk.nblk + (blk - kLag), (int)gridDim.x, st.faults,
                              false);
+#endif
             __syncwarp();
             if (wl == 0) MQ_T1(1);
         }
