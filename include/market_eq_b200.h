@@ -33,7 +33,7 @@ extern "C" {
 #endif
 
 #define MQ_ABI_VERSION 1
-#define MQ_TILE_ENTRIES 2048 /* entries staged per shared-memory tile      */
+#define MQ_TILE_ENTRIES 2048 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
 
@@ -82,8 +82,8 @@ typedef struct mq_state {
     double *cs;       /* [m]   colsum(x^k)                                     */
     double *cs_prev;  /* [m]   colsum(x^{k-1})                                 */
     double *csbar;    /* [m]   colsum(xbar)                                    */
-    int32_t *blk_done;/* [2*nblk] per block: tiles solved, column-sum warps done
-                         (zeroed per launch)                                   */
+    int32_t *blk_done;/* [2*nblk+1] per block: tiles solved, column sums done;
+                         then the dynamic tile counter (zeroed per launch)     */
     const double *steps; /* [2] tau, sigma (device-resident: one graph serves
                             every step size)                                   */
     int64_t *navg;    /* [1]  inner iterations since the last restart          */
@@ -192,6 +192,10 @@ int mq_gen_degrees(int64_t row0, int64_t nrows, int64_t m, int q_mode, double q,
 int mq_gen_fill(int64_t row0, int64_t nrows, int64_t m, int q_mode, double q, double alpha,
                 double dmin, unsigned long long seed, const int64_t *row_ptr, int32_t *col,
                 double *val, double *w, void *stream);
+
+/* Entries per primal tile this build was compiled for (tiles must not exceed
+ * it; MQ_TILE_ENTRIES by default). */
+int mq_tile_entries(void);
 
 /* Size in doubles of the `scratch` buffer the reduction calls need. */
 int64_t mq_scratch_doubles(void);

@@ -73,6 +73,7 @@ _SIGS = {
     "mq_gen_fill": (CINT, [I64, I64, I64, CINT, F64, F64, F64, ctypes.c_ulonglong, P, P, P, P,
                            P]),
     "mq_scratch_doubles": (I64, []),
+    "mq_tile_entries": (CINT, []),
     "mq_last_error": (ctypes.c_char_p, []),
     "mq_abi_version": (CINT, []),
 }

@@ -176,15 +176,80 @@ __device__ __forceinline__ double row_root_exact(const double *__restrict__ su,
     return s;
 }
 
+// Same iteration with the row held in registers (PER entries per lane):
+// sweeps cost no shared-memory traffic.
+template <int G, int PER>
+__device__ __forceinline__ double row_root_regs(const double (&c)[PER], const double (&u)[PER],
+                                                int len, double tw, double s0, double A,
+                                                double B, bool active_row, int *sweeps,
+                                                bool *ok) {
+    bool done = !active_row || len == 0;
+    double s = done ? 1.0 : active_root(A, B, tw);
+    int prev_cnt = len;
+    int nsw = 0;
+    auto sweep = [&](double q, double &As, double &Bs, int &cnt) {
+        double a_ = 0.0, b_ = 0.0;
+        int k_ = 0;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            if (fma(c[e], q, tw * u[e]) > 0.0 && u[e] > 0.0) {
+                a_ += u[e] * c[e];
+                b_ += u[e] * u[e];
+                ++k_;
+            }
+        }
+        As = group_sum<G>(a_);
+        Bs = group_sum<G>(b_);
+        cnt = group_sum_int<G>(k_);
+    };
+    const bool try_s0 = !done && s0 > s;
+    if (__any_sync(MQ_FULL, try_s0)) {
+        double A0, B0;
+        int k0;
+        sweep(try_s0 ? s0 : s, A0, B0, k0);
+        if (try_s0) {
+            ++nsw;
+            const double g0 = A0 + tw * B0 / s0;
+            if (g0 >= s0) {
+                s = fmax(active_root(A0, B0, tw), s0);
+                prev_cnt = k0;
+            } else if (g0 > s) {
+                s = g0;
+                prev_cnt = -1;
+            }
+        }
+    }
+    for (int k = 0; k < kMaxSweeps; ++k) {
+        if (!__any_sync(MQ_FULL, !done)) break;
+        double As, Bs;
+        int cnt;
+        sweep(s, As, Bs, cnt);
+        if (!done) {
+            ++nsw;
+            if (cnt == prev_cnt || cnt == 0) {
+                done = true;
+            } else {
+                s = fmax(active_root(As, Bs, tw), s);
+                prev_cnt = cnt;
+            }
+        }
+    }
+    *sweeps = nsw;
+    *ok = done;
+    return s;
+}
+
 // ------------------------------------------------------------ primal (fused)
-template <int ETILE, int RTILE>
+template <int ETILE, int RTILE, bool HASC>
 struct TileLayout {
     // one stage (every region 16-byte aligned for the bulk copies):
-    // u, x, xbar f64 [ETILE+2] | col i32 [ETILE+4] | row_ptr i64 [RTILE+4] | w f64 [RTILE+2]
+    // u, x, xbar, c f64 [ETILE+2] | col i32 [ETILE+4] | row_ptr i64 [RTILE+4] | w f64 [RTILE+2]
+    // (c = x - tau p[col] is written by the gather warps, not by TMA)
     static constexpr int kU = 0;
     static constexpr int kX = kU + (ETILE + 2) * 8;
     static constexpr int kXB = kX + (ETILE + 2) * 8;
-    static constexpr int kCol = kXB + (ETILE + 2) * 8;
+    static constexpr int kC = kXB + (ETILE + 2) * 8;
+    static constexpr int kCol = kC + (HASC ? (ETILE + 2) * 8 : 0);
     static constexpr int kRp = kCol + (ETILE + 4) * 4;
     static constexpr int kW = kRp + (RTILE + 4) * 8;
     static constexpr int kStage = (kW + (RTILE + 2) * 8 + 127) / 128 * 128;
@@ -224,6 +289,10 @@ __device__ __forceinline__ void aligned_span(const void *base, int64_t first, in
 }
 
 constexpr int kCsCap = 10240;         // staged bperm entries per CTA (40 KB)
+#ifndef MQ_REG_PER
+#define MQ_REG_PER 8
+#endif
+constexpr int kRegPer = MQ_REG_PER;   // entries per lane kept in registers
 constexpr int kCsCols = 1152;         // goods per CTA (>= QMAX * NCW * 32)
 #ifndef MQ_LAG
 #define MQ_LAG 4
@@ -260,30 +329,36 @@ __device__ __forceinline__ void wait_counter(const int *ctr, int target, int64_t
     if (acquire) __threadfence();
 }
 
-// Warps 0..NSW-1 solve rows, warp NSW produces (TMA), warps NSW+1..NSW+NCW sum
-// columns.  full[s]: stage s has landed; empty[s]: every solver warp is done
-// with it.  Solver warps claim row pairs from a shared counter, so no solver
-// waits for another inside a tile.
-template <int G, int NSW, int NCW, int ETILE, int RTILE, int NSTAGE, int QMAX>
-__global__ void __launch_bounds__((NSW + NCW + 1) * 32, 1)
+// Warps 0..NSW-1 solve rows, warp NSW produces (TMA), warps NSW+1..NSW+NGW
+// gather prices (c = x - tau p[col] for the whole tile), the last NCW warps
+// sum columns.  full[s]: stage s has landed; ready[s]: its c is computed;
+// empty[s]: every solver warp is done with it.  Solver warps claim row pairs
+// from a shared counter, so no solver waits for another inside a tile, and
+// they never touch global memory before their stores.
+template <int G, int NSW, int NGW, int NCW, int ETILE, int RTILE, int NSTAGE, int QMAX>
+__global__ void __launch_bounds__((NSW + NGW + NCW + 1) * 32, 1)
 primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
                     int write_cs) {
-    using L = TileLayout<ETILE, RTILE>;
+    using L = TileLayout<ETILE, RTILE, (NGW > 0)>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTAGE * L::kStage);
     uint64_t *empty = full + NSTAGE;
-    int *claim = reinterpret_cast<int *>(empty + NSTAGE);
-    int32_t *cstage = reinterpret_cast<int32_t *>(claim + 4 * NSTAGE);  // column-sum staging
+    uint64_t *ready = empty + NSTAGE;
+    int64_t *stile = reinterpret_cast<int64_t *>(ready + NSTAGE);  // tile held by each stage
+    int *claim = reinterpret_cast<int *>(stile + NSTAGE);
+    // column-sum staging (16-byte aligned: TMA bulk-copy destination)
+    int32_t *cstage = reinterpret_cast<int32_t *>(
+        (reinterpret_cast<uintptr_t>(claim + 4 * NSTAGE) + 127) & ~uintptr_t(127));
     constexpr int GPW = 32 / G;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, wl = tid & 31;
-    const int64_t first = blockIdx.x, stride = gridDim.x;
     const int64_t tpb_all = mk.tiles_per_block;  // tiles per block (all CTAs)
 
     if (tid == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NSW);
+            mbar_init(&ready[s], NGW > 0 ? NGW : 1);
         }
         mbar_fence_init();
     }
@@ -296,18 +371,26 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 __threadfence();
                 atomicAdd(&st.blk_done[k / tpb_all], 1);
             };
+            // tiles are claimed dynamically (global counter) so that every block
+            // of tiles completes with little skew across CTAs
+            int *tile_ctr = st.blk_done + 2 * mk.nblk;
             int64_t j = 0;
             for (;; ++j) {
-                const int64_t k = first + j * stride;
-                if (k >= mk.ntiles) break;
                 const int s = (int)(j % NSTAGE);
                 if (j >= NSTAGE) {
                     MQ_T0();
                     mbar_wait(&empty[s], (uint32_t)(((j / NSTAGE) - 1) & 1));
                     MQ_T1(2);
-                    finished(first + (j - NSTAGE) * stride);
+                    finished(stile[s]);
                 }
+                const int64_t k = atomicAdd(tile_ctr, 1);
                 claim[s] = 0;
+                if (k >= mk.ntiles) {  // sentinel: consumers leave
+                    stile[s] = -1;
+                    mbar_expect_tx(&full[s], 0);
+                    break;
+                }
+                stile[s] = k;
                 fence_proxy_async();
                 const int64_t r0 = mk.tiles[2 * k], r1 = mk.tiles[2 * k + 1];
                 const int64_t e0 = mk.row_ptr[r0], cnt = mk.row_ptr[r1] - e0;
@@ -330,27 +413,71 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     bulk_g2s_hint(base + L::kCol, src_c, b4, &full[s], pol);
                 }
             }
-            // drain: the last (up to NSTAGE) tiles
-            for (int64_t jj = (j > NSTAGE ? j - NSTAGE : 0); jj < j; ++jj) {
+            // drain: tiles still held by the other stages
+            for (int64_t jj = (j >= NSTAGE - 1 ? j - NSTAGE + 1 : 0); jj < j; ++jj) {
                 const int s = (int)(jj % NSTAGE);
                 mbar_wait(&empty[s], (uint32_t)((jj / NSTAGE) & 1));
-                finished(first + jj * stride);
+                finished(stile[s]);
             }
         }
         return;
     }
 
+    const double tau = st.steps[0];
+    if (NGW > 0 && warp > NSW && warp <= NSW + NGW) {  // -------------- price gather
+        const int gt = tid - (NSW + 1) * 32;
+        for (int64_t j = 0;; ++j) {
+            const int s = (int)(j % NSTAGE);
+            mbar_wait(&full[s], (uint32_t)((j / NSTAGE) & 1));
+            const int64_t k = stile[s];
+            if (k >= 0) {
+                unsigned char *base = smem + s * L::kStage;
+                const int64_t r0 = mk.tiles[2 * k];
+                const int lr = (int)(((r0 * 8) & 15) >> 3);
+                const int64_t *srp = reinterpret_cast<const int64_t *>(base + L::kRp) + lr;
+                const int nrows = (int)(mk.tiles[2 * k + 1] - r0);
+                const int64_t e0 = srp[0];
+                const int cnt = (int)(srp[nrows] - e0);
+                const int d8 = (int)(((e0 * 8) & 15) >> 3), d4 = (int)(((e0 * 4) & 15) >> 2);
+                const double *sx = reinterpret_cast<const double *>(base + L::kX) + d8;
+                double *sc = reinterpret_cast<double *>(base + L::kC) + d8;
+                const int32_t *scol = reinterpret_cast<const int32_t *>(base + L::kCol) + d4;
+                constexpr int U = 4;
+                for (int t0 = gt; t0 < cnt; t0 += NGW * 32 * U) {
+                    double pv[U];
+#pragma unroll
+                    for (int q = 0; q < U; ++q) {
+                        const int t = t0 + q * NGW * 32;
+                        pv[q] = t < cnt ? __ldg(st.p + scol[t]) : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < U; ++q) {
+                        const int t = t0 + q * NGW * 32;
+                        if (t < cnt) {
+                            const double xe = sx[t];
+                            sc[t] = xe - tau * pv[q];
+                            if (x_prev_out) x_prev_out[e0 + t] = xe;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (wl == 0) mbar_arrive(&ready[s]);
+            if (k < 0) break;
+        }
+        return;
+    }
 #ifdef MQ_NO_COLSUM  // timing experiment only: solver without column sums
-    if (warp > NSW) return;
+    if (warp > NSW + NGW) return;
 #endif
-    if (warp > NSW) {  // ---------------------------------------- column sums
+    if (warp > NSW + NGW) {  // ---------------------------------- column sums
         // The CTA's NCW column-sum warps own goods [j_lo, j_hi); thread ct owns
         // j_lo + ct + q*NCW*32.  Per block, one thread stages the block's
         // schedule slice (bptr for the owned goods, their bperm range) into
         // shared memory with TMA bulk copies, issued before the block is even
         // solved; once every CTA has solved the block, each thread gathers its
         // goods' x values from L2 and adds them in ascending row order.
-        const int ct = tid - (NSW + 1) * 32;
+        const int ct = tid - (NSW + NGW + 1) * 32;
         const int64_t per = (mk.m + gridDim.x - 1) / gridDim.x;
         const int64_t j_lo = blockIdx.x * per;
         const int64_t j_hi = j_lo + per < mk.m ? j_lo + per : mk.m;
@@ -469,14 +596,18 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
     // ---------------------------------------------------------- solvers
     const int lane = tid & (G - 1);
     const int gsub = wl / G;
-    const double tau = st.steps[0];
     const Avg av = avg_weights(st.navg, it);
     int64_t my_sweeps = 0;
     int64_t my_faults = 0;
     for (int64_t j = 0;; ++j) {
-        const int64_t k = first + j * stride;
-        if (k >= mk.ntiles) break;
         const int s = (int)(j % NSTAGE);
+        {
+            MQ_T0();
+            mbar_wait(NGW > 0 ? &ready[s] : &full[s], (uint32_t)((j / NSTAGE) & 1));
+            if (wl == 0) MQ_T1(0);
+        }
+        const int64_t k = stile[s];
+        if (k < 0) break;  // sentinel
         // throttle: stay within kLag blocks of the column-sum front, so the
         // blocks still to be gathered are L2-resident
         const int64_t blk = k / tpb_all;
@@ -490,11 +621,6 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             __syncwarp();
             if (wl == 0) MQ_T1(1);
         }
-        {
-            MQ_T0();
-            mbar_wait(&full[s], (uint32_t)((j / NSTAGE) & 1));
-            if (wl == 0) MQ_T1(0);
-        }
         const int64_t r0 = mk.tiles[2 * k], r1 = mk.tiles[2 * k + 1];
         const int nrows = (int)(r1 - r0);
         unsigned char *base = smem + s * L::kStage;
@@ -504,8 +630,11 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         const int64_t e0 = srp[0];
         const int d8 = (int)(((e0 * 8) & 15) >> 3), d4 = (int)(((e0 * 4) & 15) >> 2);
         const double *su = reinterpret_cast<const double *>(base + L::kU) + d8;
-        double *sx = reinterpret_cast<double *>(base + L::kX) + d8;  // x, then c in place
+        double *sx = reinterpret_cast<double *>(base + L::kX) + d8;
         const double *sxb = reinterpret_cast<const double *>(base + L::kXB) + d8;
+        // c = x - tau p[col]: from the gather warps, or computed here (then
+        // written over x in place for the shared-memory path)
+        double *sc = reinterpret_cast<double *>(base + (NGW > 0 ? L::kC : L::kX)) + d8;
         const int32_t *scol = reinterpret_cast<const int32_t *>(base + L::kCol) + d4;
 
         for (;;) {
@@ -522,44 +651,82 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 b = (int)(srp[r + 1] - e0);
                 tw = tau * sw[r];
             }
-            MQ_T0();
-            double s0p = 0.0, ap = 0.0, bp = 0.0;
-            for (int t = a + lane; t < b; t += G) {
-                const double ue = su[t], xe = sx[t];
-                const double ce = xe - tau * __ldg(st.p + scol[t]);
-                if (x_prev_out) x_prev_out[e0 + t] = xe;
-                sx[t] = ce;
-                s0p += ue * xe;
-                ap += ue * ce;
-                bp += ue * ue;
+            int nsw = 0;
+            bool ok = true;
+            if (__all_sync(MQ_FULL, b - a <= kRegPer * G)) {
+                // ---- row in registers
+                double c[kRegPer], u[kRegPer];
+                double s0p = 0.0, ap = 0.0, bp = 0.0;
+#pragma unroll
+                for (int e = 0; e < kRegPer; ++e) {
+                    const int t = a + lane + e * G;
+                    if (t < b) {
+                        const double ue = su[t], xe = sx[t];
+                        double ce;
+                        if (NGW > 0) {
+                            ce = sc[t];
+                        } else {
+                            ce = xe - tau * __ldg(st.p + scol[t]);
+                            if (x_prev_out) x_prev_out[e0 + t] = xe;
+                        }
+                        u[e] = ue;
+                        c[e] = ce;
+                        s0p += ue * xe;
+                        ap += ue * ce;
+                        bp += ue * ue;
+                    } else {
+                        u[e] = 0.0;
+                        c[e] = 0.0;
+                    }
+                }
+                const double s0 = group_sum<G>(s0p);
+                const double A = group_sum<G>(ap);
+                const double B = group_sum<G>(bp);
+                const double sr =
+                    row_root_regs<G, kRegPer>(c, u, b - a, tw, s0, A, B, has, &nsw, &ok);
+                const double inv_s = 1.0 / sr;
+#pragma unroll
+                for (int e = 0; e < kRegPer; ++e) {
+                    const int t = a + lane + e * G;
+                    if (t < b) {
+                        const double xn = fmax(c[e] + tw * u[e] * inv_s, 0.0);
+                        st.x[e0 + t] = xn;
+                        __stcs(st.xbar + e0 + t, av.wold * sxb[t] + av.wnew * xn);
+                    }
+                }
+            } else {
+                // ---- longer rows: stream the row from shared memory
+                double s0p = 0.0, ap = 0.0, bp = 0.0;
+                for (int t = a + lane; t < b; t += G) {
+                    const double ue = su[t], xe = sx[t];
+                    double ce;
+                    if (NGW > 0) {
+                        ce = sc[t];
+                    } else {
+                        ce = xe - tau * __ldg(st.p + scol[t]);
+                        if (x_prev_out) x_prev_out[e0 + t] = xe;
+                        sc[t] = ce;  // == sx[t]: this lane's entry only
+                    }
+                    s0p += ue * xe;
+                    ap += ue * ce;
+                    bp += ue * ue;
+                }
+                const double s0 = group_sum<G>(s0p);
+                const double A = group_sum<G>(ap);
+                const double B = group_sum<G>(bp);
+                const double sr =
+                    row_root_exact<G>(su, sc, a, b, lane, tw, s0, A, B, has, &nsw, &ok);
+                const double inv_s = 1.0 / sr;
+                for (int t = a + lane; t < b; t += G) {
+                    const double xn = fmax(sc[t] + tw * su[t] * inv_s, 0.0);
+                    st.x[e0 + t] = xn;
+                    __stcs(st.xbar + e0 + t, av.wold * sxb[t] + av.wnew * xn);
+                }
             }
-            const double s0 = group_sum<G>(s0p);
-            const double A = group_sum<G>(ap);
-            const double B = group_sum<G>(bp);
-            if (wl == 0) MQ_T1(5);
-            int nsw;
-            bool ok;
-#ifdef MQ_PROFILE_WAITS
-            const long long _t1 = clock64();
-#endif
-            const double sr = row_root_exact<G>(su, sx, a, b, lane, tw, s0, A, B, has, &nsw, &ok);
-#ifdef MQ_PROFILE_WAITS
-            if (wl == 0) atomicAdd(&g_wait_cycles[6], (unsigned long long)(clock64() - _t1));
-            const long long _t2 = clock64();
-#endif
             if (has && b > a && lane == 0) {
                 my_sweeps += nsw;
                 if (!ok) ++my_faults;
             }
-            const double inv_s = 1.0 / sr;
-            for (int t = a + lane; t < b; t += G) {
-                const double xn = fmax(sx[t] + tw * su[t] * inv_s, 0.0);
-                st.x[e0 + t] = xn;
-                __stcs(st.xbar + e0 + t, av.wold * sxb[t] + av.wnew * xn);
-            }
-#ifdef MQ_PROFILE_WAITS
-            if (wl == 0) atomicAdd(&g_wait_cycles[7], (unsigned long long)(clock64() - _t2));
-#endif
         }
         __syncwarp();
         if (wl == 0) mbar_arrive(&empty[s]);
@@ -745,21 +912,31 @@ static int sm_count() {
 #define MQ_G 16
 #endif
 #ifndef MQ_NCW
-#define MQ_NCW 6
+#define MQ_NCW 4
 #endif
 #ifndef MQ_NSW
-#define MQ_NSW 16
+#define MQ_NSW 15
 #endif
-constexpr int kG = MQ_G, kNSW = MQ_NSW, kNCW = MQ_NCW, kStages = 3;
+#ifndef MQ_NGW
+#define MQ_NGW 0
+#endif
+#ifndef MQ_ETILE
+#define MQ_ETILE MQ_TILE_ENTRIES
+#endif
+#ifndef MQ_STAGES
+#define MQ_STAGES 3
+#endif
+constexpr int kG = MQ_G, kNSW = MQ_NSW, kNGW = MQ_NGW, kNCW = MQ_NCW, kStages = MQ_STAGES;
+constexpr int kEtile = MQ_ETILE;
 constexpr int kQMax = (1152 + kNCW * 32 - 1) / (kNCW * 32);
-using PrimalLayout = TileLayout<MQ_TILE_ENTRIES, MQ_TILE_ROWS>;
+using PrimalLayout = TileLayout<kEtile, MQ_TILE_ROWS, (kNGW > 0)>;
 static_assert(kQMax * kNCW * 32 >= kCsCols, "column-sum threads cannot cover a slice");
-constexpr int kPrimalSmem = kStages * PrimalLayout::kStage + 2 * kStages * 8 + 4 * kStages * 4 +
+constexpr int kPrimalSmem = kStages * PrimalLayout::kStage + 4 * kStages * 8 + 4 * kStages * 4 + 128 +
                             (kCsCap + kCsCols + 8) * 4 + 4 * 8 + 16;
 
 int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev, cudaStream_t s) {
     static bool configured = false;
-    auto kern = primal_fused_kernel<kG, kNSW, kNCW, MQ_TILE_ENTRIES, MQ_TILE_ROWS, kStages, kQMax>;
+    auto kern = primal_fused_kernel<kG, kNSW, kNGW, kNCW, kEtile, MQ_TILE_ROWS, kStages, kQMax>;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kPrimalSmem);
@@ -769,8 +946,9 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
     if (mk->ntiles > 0) {
         if ((mk->m + mk->prim_grid - 1) / mk->prim_grid > (int64_t)kCsCols)
             return set_error(cudaErrorInvalidValue, "mq_primal_step: too many goods per CTA");
-        cudaMemsetAsync(st->blk_done, 0, sizeof(int32_t) * 2 * (size_t)mk->nblk, s);
-        kern<<<mk->prim_grid, (kNSW + kNCW + 1) * 32, kPrimalSmem, s>>>(*mk, *st, it, xprev, 1);
+        cudaMemsetAsync(st->blk_done, 0, sizeof(int32_t) * (2 * (size_t)mk->nblk + 1), s);
+        kern<<<mk->prim_grid, (kNSW + kNGW + kNCW + 1) * 32, kPrimalSmem, s>>>(*mk, *st, it,
+                                                                                xprev, 1);
     } else {
         cudaMemsetAsync(st->cs, 0, sizeof(double) * (size_t)mk->m, s);
     }
@@ -854,6 +1032,8 @@ int mq_debug_counters(unsigned long long *out_host) {
     e = cudaMemcpyToSymbol(g_wait_cycles, z, sizeof(z));
     return e == cudaSuccess ? 0 : set_error(e, "mq_debug_counters");
 }
+
+int mq_tile_entries(void) { return kEtile; }
 
 int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream) {
     const int grid = (int)((mk->m + 255) / 256);

@@ -181,7 +181,9 @@ class DeviceMarket:
             self.col_counts = (torch.bincount(self.col.to(torch.int64), minlength=self.m)
                                if self.nnz else torch.zeros(self.m, dtype=torch.int64,
                                                             device=dev))
-            self.tiles, self.long_rows = build_tiles(self.row_ptr)
+            etile = int(self.lib.mq_tile_entries())
+            self.tiles, self.long_rows = build_tiles(self.row_ptr, etile,
+                                                     min(nat.LONG_ROW, etile // 2))
             self.prim_grid = int(min(max(1, self.tiles.shape[0]), sm_count(dev)))
             self.bperm, self.bptr, self.nblk, self.tiles_per_block = build_blocked_schedule(
                 self.row_ptr, self.col, self.m, self.tiles, self.long_rows, self.prim_grid)

@@ -131,7 +131,7 @@ class PdhcgEngine:
         self.xbar = self._xbar_buf[:nnz]
         self.x0 = torch.zeros(nnz, **f64)
         # per block: tiles solved, then column-sum warps done (throttle)
-        self.blk_done = torch.zeros(max(1, 2 * dm.nblk), dtype=torch.int32, device=dev)
+        self.blk_done = torch.zeros(2 * dm.nblk + 1, dtype=torch.int32, device=dev)
         self.p = torch.zeros(m, **f64)
         self.pbar = torch.zeros(m, **f64)
         self.p0 = torch.zeros(m, **f64)
