@@ -277,7 +277,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-max-iters", type=int, default=6000)
+    ap.add_argument("--e2e-max-iters", type=int, default=2000)
     ap.add_argument("--breakdown-iters", type=int, default=20)
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
@@ -335,7 +335,9 @@ def main():
     # per-kernel breakdown and the primal kernel's roofline
     kt, kpass = kernel_breakdown(eng, a.breakdown_iters)
     n_local = dm.n
-    primal_bytes = 44 * nnz_local + 20 * n_local + 8 * m
+    # fused kernel = prox + averages (44 B/nnz + 20 B/row + p) and the column
+    # sums of the new x (bperm 4 + x 8 B/nnz): DESIGN.md §5.1
+    primal_bytes = 56 * nnz_local + 20 * n_local + 8 * m
     achieved = primal_bytes / (kt[1] / 1e3) / 1e9
     iter_bytes = 56 * nnz_full + 16 * n_full + 48 * m      # SURVEY §8(d) B_iter
     iter_gbs = iter_bytes / (t_ms / 1e3 / a.steps) / 1e9 / world
@@ -350,7 +352,8 @@ def main():
                    "row_solver": "exact", "parallelism": f"row-shard x{world}",
                    "l2": f"inputs larger than L2 ({iter_bytes / 1e9:.1f} GB algorithmic "
                          "traffic per iteration vs 126 MB L2)"},
-        "roofline": {"bound": "hbm", "kernel": "primal (exact prox + average)",
+        "roofline": {"bound": "hbm",
+                     "kernel": "primal_fused_kernel (exact prox + averages + column sums)",
                      "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4),
                      "traffic": traffic_from_profile("primal"), "peak_kind": peak_kind,

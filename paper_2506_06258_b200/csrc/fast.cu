@@ -68,7 +68,20 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
+#ifndef MQ_WAIT_HINT_NS
+#define MQ_WAIT_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#if MQ_WAIT_HINT_NS > 0
+    // suspend-time hint: a waiting warp sleeps instead of re-polling shared memory
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "MQ_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra MQ_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity), "n"(MQ_WAIT_HINT_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "MQ_WAIT_%=:\n\t"
@@ -76,6 +89,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "@!p bra MQ_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
         "r"(parity)
         : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
                                          uint64_t *bar) {

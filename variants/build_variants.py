@@ -5,10 +5,9 @@ from paper_2506_06258_b200 import _build
 HERE = os.path.dirname(os.path.abspath(__file__))
 V = {
   "base": dict(),
-  "nocolsum": dict(MQ_NO_COLSUM=1),
-  "gw": dict(MQ_NSW=12, MQ_NGW=4, MQ_NCW=3, MQ_STAGES=2),
-  "lag8": dict(MQ_LAG=8),
-  "c6s13": dict(MQ_NSW=13, MQ_NCW=6),
+  "hint1000": dict(MQ_WAIT_HINT_NS=1000),
+  "hint10000": dict(MQ_WAIT_HINT_NS=10000),
+  "hint1000_nocs": dict(MQ_WAIT_HINT_NS=1000, MQ_NO_COLSUM=1),
 }
 for name, d in V.items():
     flags = [f"-D{k}={v}" for k, v in d.items()]
