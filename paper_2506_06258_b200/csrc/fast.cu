@@ -667,12 +667,13 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             }
             int nsw = 0;
             bool ok = true;
-            if (__all_sync(MQ_FULL, b - a <= kRegPer * G)) {
+            if (kRegPer > 0 && __all_sync(MQ_FULL, b - a <= kRegPer * G)) {
                 // ---- row in registers
-                double c[kRegPer], u[kRegPer];
+                constexpr int RP = kRegPer > 0 ? kRegPer : 1;
+                double c[RP], u[RP];
                 double s0p = 0.0, ap = 0.0, bp = 0.0;
 #pragma unroll
-                for (int e = 0; e < kRegPer; ++e) {
+                for (int e = 0; e < RP; ++e) {
                     const int t = a + lane + e * G;
                     if (t < b) {
                         const double ue = su[t], xe = sx[t];
@@ -697,10 +698,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 const double A = group_sum<G>(ap);
                 const double B = group_sum<G>(bp);
                 const double sr =
-                    row_root_regs<G, kRegPer>(c, u, b - a, tw, s0, A, B, has, &nsw, &ok);
+                    row_root_regs<G, RP>(c, u, b - a, tw, s0, A, B, has, &nsw, &ok);
                 const double inv_s = 1.0 / sr;
 #pragma unroll
-                for (int e = 0; e < kRegPer; ++e) {
+                for (int e = 0; e < RP; ++e) {
                     const int t = a + lane + e * G;
                     if (t < b) {
                         const double xn = fmax(c[e] + tw * u[e] * inv_s, 0.0);

@@ -5,9 +5,11 @@ from paper_2506_06258_b200 import _build
 HERE = os.path.dirname(os.path.abspath(__file__))
 V = {
   "base": dict(),
-  "hint1000": dict(MQ_WAIT_HINT_NS=1000),
-  "hint10000": dict(MQ_WAIT_HINT_NS=10000),
-  "hint1000_nocs": dict(MQ_WAIT_HINT_NS=1000, MQ_NO_COLSUM=1),
+  "r0s15": dict(MQ_REG_PER=0),
+  "r0s27c4": dict(MQ_REG_PER=0, MQ_NSW=27, MQ_NCW=4),
+  "r0s23c8": dict(MQ_REG_PER=0, MQ_NSW=23, MQ_NCW=8),
+  "r0s27_nocs": dict(MQ_REG_PER=0, MQ_NSW=27, MQ_NCW=4, MQ_NO_COLSUM=1),
+  "r0s19c4": dict(MQ_REG_PER=0, MQ_NSW=19, MQ_NCW=4),
 }
 for name, d in V.items():
     flags = [f"-D{k}={v}" for k, v in d.items()]
