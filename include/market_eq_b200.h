@@ -48,9 +48,9 @@ typedef struct mq_market {
                                 instance.py:118-138                             */
     const double *u_orig;    /* [nnz] original utilities (residuals, kkt.py)    */
     const double *w;         /* [n] [pad] budgets                               */
-    /* row tiles of the primal kernel: tile k = rows [tiles[2k], tiles[2k+1]),
-       at most MQ_TILE_ENTRIES entries and MQ_TILE_ROWS rows, no row longer
-       than MQ_LONG_ROW                                                       */
+    /* row tiles of the primal kernel: tile k = rows [tiles[4k], tiles[4k+1])
+       = entries [tiles[4k+2], tiles[4k+3]), at most MQ_TILE_ENTRIES entries
+       and MQ_TILE_ROWS rows, no row longer than MQ_LONG_ROW (32-byte aligned) */
     const int64_t *tiles;
     int64_t ntiles;
     const int32_t *long_rows; /* rows longer than MQ_LONG_ROW                   */
@@ -67,6 +67,11 @@ typedef struct mq_market {
     const int32_t *bptr;     /* [(nblk+1)*m + 1]                                */
     int64_t nblk, tiles_per_block;
     int32_t prim_grid;       /* CTAs of the persistent primal kernel            */
+    /* column-major positions (scatter mode): entry e is the tpos[e]-th entry
+       of the reference's transpose schedule (sparse.py:130-145); good j owns
+       positions [tptr[j], tptr[j+1]) of that order                           */
+    const int32_t *tpos;     /* [nnz] [pad]                                     */
+    const int64_t *tptr;     /* [m+1]                                           */
     int64_t row_begin;       /* first global row of this shard (0 on 1 GPU)    */
 } mq_market;
 
@@ -84,6 +89,7 @@ typedef struct mq_state {
     double *csbar;    /* [m]   colsum(xbar)                                    */
     int32_t *blk_done;/* [2*nblk+1] per block: tiles solved, column sums done;
                          then the dynamic tile counter (zeroed per launch)     */
+    double *xc;       /* [nnz] x in column-major order (scatter mode)          */
     const double *steps; /* [2] tau, sigma (device-resident: one graph serves
                             every step size)                                   */
     int64_t *navg;    /* [1]  inner iterations since the last restart          */
@@ -196,6 +202,14 @@ int mq_gen_fill(int64_t row0, int64_t nrows, int64_t m, int q_mode, double q, do
 /* Entries per primal tile this build was compiled for (tiles must not exceed
  * it; MQ_TILE_ENTRIES by default). */
 int mq_tile_entries(void);
+
+/* How this build computes the price step's column sums: 0 = gathered from L2
+ * inside the persistent primal kernel by column-sum warps, 1 = scattered by
+ * mq_primal_step into st->xc (column-major, needs mk->tpos / mk->tptr) and
+ * streamed by mq_colsum_step, 2 (default) = per block of tiles, a primal
+ * launch followed by a gather launch over the block's schedule while its x is
+ * L2-resident. */
+int mq_colsum_mode(void);
 
 /* Size in doubles of the `scratch` buffer the reduction calls need. */
 int64_t mq_scratch_doubles(void);

@@ -25,6 +25,47 @@
 //    pass and overlap the streaming.
 #include "mq_common.cuh"
 
+// ---- compile-time configuration (tuning variants override with -D) ----
+#ifndef MQ_G
+#define MQ_G 16
+#endif
+#ifndef MQ_NCW
+#define MQ_NCW 4
+#endif
+#ifndef MQ_NSW
+#define MQ_NSW 15
+#endif
+#ifndef MQ_NGW
+#define MQ_NGW 0
+#endif
+#ifndef MQ_ETILE
+#define MQ_ETILE MQ_TILE_ENTRIES
+#endif
+#ifndef MQ_STAGES
+#define MQ_STAGES 3
+#endif
+#ifndef MQ_LAG
+#define MQ_LAG 4
+#endif
+#ifndef MQ_REG_PER
+#define MQ_REG_PER 8
+#endif
+#ifndef MQ_CLAIM
+#define MQ_CLAIM 2
+#endif
+#ifndef MQ_CSQ
+#define MQ_CSQ 4
+#endif
+#ifndef MQ_CSU
+#define MQ_CSU 8
+#endif
+#ifndef MQ_CS_CHUNK
+#define MQ_CS_CHUNK 512
+#endif
+#ifndef MQ_WAIT_HINT_NS
+#define MQ_WAIT_HINT_NS 0
+#endif
+
 namespace mq {
 
 constexpr int kMaxSweeps = 4096;
@@ -68,9 +109,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
-#ifndef MQ_WAIT_HINT_NS
-#define MQ_WAIT_HINT_NS 0
-#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 #if MQ_WAIT_HINT_NS > 0
     // suspend-time hint: a waiting warp sleeps instead of re-polling shared memory
@@ -254,6 +292,17 @@ __device__ __forceinline__ double row_root_regs(const double (&c)[PER], const do
 }
 
 // ------------------------------------------------------------ primal (fused)
+#ifdef MQ_SCATTER
+constexpr bool kScatter = true;       // column sums from a column-major copy of x
+#else
+constexpr bool kScatter = false;
+#endif
+#ifdef MQ_COLSUM_SPLIT
+constexpr bool kSplit = !kScatter;    // per block of tiles: primal launch, then gather launch
+#else
+constexpr bool kSplit = false;        // column sums gathered in-kernel (column-sum warps)
+#endif
+
 template <int ETILE, int RTILE, bool HASC>
 struct TileLayout {
     // one stage (every region 16-byte aligned for the bulk copies):
@@ -264,7 +313,8 @@ struct TileLayout {
     static constexpr int kXB = kX + (ETILE + 2) * 8;
     static constexpr int kC = kXB + (ETILE + 2) * 8;
     static constexpr int kCol = kC + (HASC ? (ETILE + 2) * 8 : 0);
-    static constexpr int kRp = kCol + (ETILE + 4) * 4;
+    static constexpr int kTp = kCol + (ETILE + 4) * 4;       // tpos (scatter mode)
+    static constexpr int kRp = kTp + (kScatter ? (ETILE + 4) * 4 : 0);
     static constexpr int kW = kRp + (RTILE + 4) * 8;
     static constexpr int kStage = (kW + (RTILE + 2) * 8 + 127) / 128 * 128;
     static_assert(kX % 16 == 0 && kCol % 16 == 0 && kRp % 16 == 0 && kW % 16 == 0,
@@ -287,6 +337,15 @@ __device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32
         "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
         : "memory");
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// scatter store kept in L2 until its 32-byte sector is complete
+__device__ __forceinline__ void st_keep(double *p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ int ld_acquire(const int *p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -302,15 +361,23 @@ __device__ __forceinline__ void aligned_span(const void *base, int64_t first, in
     *bytes = (uint32_t)((d + count * S + 15) & ~(int64_t)15);
 }
 
-constexpr int kCsCap = 10240;         // staged bperm entries per CTA (40 KB)
-#ifndef MQ_REG_PER
-#define MQ_REG_PER 8
+#ifdef MQ_CS_PERWARP
+constexpr bool kCsPerWarp = true;     // each column-sum warp publishes its progress
+#else
+constexpr bool kCsPerWarp = false;    // one publication per CTA
 #endif
+constexpr int kCsCap = 10240;         // staged bperm entries per CTA (CTA-level column sums)
+constexpr int kCsChunk = MQ_CS_CHUNK; // bperm entries per staged column-sum chunk (per warp)
+constexpr int kWCols = MQ_NCW >= 4 ? 320 : 600;  // goods per column-sum warp
+constexpr int kClaim = MQ_CLAIM;      // tiles claimed per atomic by a producer
 constexpr int kRegPer = MQ_REG_PER;   // entries per lane kept in registers
-constexpr int kCsCols = 1152;         // goods per CTA (>= QMAX * NCW * 32)
-#ifndef MQ_LAG
-#define MQ_LAG 4
+#ifdef MQ_TRIVIAL_SOLVE
+constexpr bool kTrivial = true;       // bandwidth experiments only
+#else
+constexpr bool kTrivial = false;
 #endif
+constexpr int kCsCols = 1152;         // goods per CTA (>= QMAX * NCW * 32)
+constexpr int kCsQ = MQ_CSQ, kCsU = MQ_CSU;  // goods x gathers in flight per column-sum thread
 constexpr int64_t kLag = MQ_LAG;      // solver blocks ahead of the slowest column-sum CTA
 constexpr int64_t kSpinLimit = 4000000000ll;  // ~2 s of clock64: a stalled block is a fault
 
@@ -352,14 +419,15 @@ __device__ __forceinline__ void wait_counter(const int *ctr, int target, int64_t
 template <int G, int NSW, int NGW, int NCW, int ETILE, int RTILE, int NSTAGE, int QMAX>
 __global__ void __launch_bounds__((NSW + NGW + NCW + 1) * 32, 1)
 primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
-                    int write_cs) {
+                    int write_cs, int64_t tile_lo, int64_t tile_hi, int *tile_ctr) {
     using L = TileLayout<ETILE, RTILE, (NGW > 0)>;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTAGE * L::kStage);
     uint64_t *empty = full + NSTAGE;
     uint64_t *ready = empty + NSTAGE;
     int64_t *stile = reinterpret_cast<int64_t *>(ready + NSTAGE);  // tile held by each stage
-    int *claim = reinterpret_cast<int *>(stile + NSTAGE);
+    int64_t *smeta = stile + NSTAGE;                               // its r0, r1, e0 per stage
+    int *claim = reinterpret_cast<int *>(smeta + 3 * NSTAGE);
     // column-sum staging (16-byte aligned: TMA bulk-copy destination)
     int32_t *cstage = reinterpret_cast<int32_t *>(
         (reinterpret_cast<uintptr_t>(claim + 4 * NSTAGE) + 127) & ~uintptr_t(127));
@@ -381,33 +449,58 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
     if (warp == NSW) {  // ---------------------------------------- producer
         if (wl == 0) {
             const uint64_t pol = policy_evict_first();
-            auto finished = [&](int64_t k) {  // tile k fully written by this CTA
-                __threadfence();
-                atomicAdd(&st.blk_done[k / tpb_all], 1);
+            // tiles are claimed dynamically (global counter, kClaim at a time) so
+            // that every block of tiles completes with little skew across CTAs;
+            // the next tile's claim and metadata are fetched one step ahead so
+            // the producer never waits on a dependent global load
+            int64_t batch = tile_lo + atomicAdd(tile_ctr, kClaim);
+            int bpos = 0;
+            auto next_tile = [&]() -> int64_t {
+                if (bpos == kClaim) {
+                    batch = tile_lo + atomicAdd(tile_ctr, kClaim);
+                    bpos = 0;
+                }
+                return batch + bpos++;
             };
-            // tiles are claimed dynamically (global counter) so that every block
-            // of tiles completes with little skew across CTAs
-            int *tile_ctr = st.blk_done + 2 * mk.nblk;
+            auto load_meta = [&](int64_t k, longlong2 &a01, longlong2 &a23) {
+                if (k < tile_hi) {
+                    const longlong2 *tp = reinterpret_cast<const longlong2 *>(mk.tiles + 4 * k);
+                    a01 = __ldg(tp);
+                    a23 = __ldg(tp + 1);
+                }
+            };
+            int64_t kn = next_tile();
+            longlong2 mn01 = {0, 0}, mn23 = {0, 0};
+            load_meta(kn, mn01, mn23);
             int64_t j = 0;
             for (;; ++j) {
                 const int s = (int)(j % NSTAGE);
+                const int64_t k = kn;
+                const longlong2 m01 = mn01, m23 = mn23;
+                if (k < tile_hi) {
+                    kn = next_tile();
+                    load_meta(kn, mn01, mn23);
+                }
                 if (j >= NSTAGE) {
                     MQ_T0();
                     mbar_wait(&empty[s], (uint32_t)(((j / NSTAGE) - 1) & 1));
                     MQ_T1(2);
-                    finished(stile[s]);
                 }
-                const int64_t k = atomicAdd(tile_ctr, 1);
                 claim[s] = 0;
-                if (k >= mk.ntiles) {  // sentinel: consumers leave
+                claim[NSTAGE + s] = 0;  // solver warps done with this use
+                if (k >= tile_hi) {  // sentinel: consumers leave
                     stile[s] = -1;
                     mbar_expect_tx(&full[s], 0);
                     break;
                 }
+                const int64_t r0 = m01.x, r1 = m01.y, e0 = m23.x, cnt = m23.y - m23.x;
                 stile[s] = k;
-                fence_proxy_async();
-                const int64_t r0 = mk.tiles[2 * k], r1 = mk.tiles[2 * k + 1];
-                const int64_t e0 = mk.row_ptr[r0], cnt = mk.row_ptr[r1] - e0;
+                smeta[3 * s] = r0;
+                smeta[3 * s + 1] = r1;
+                smeta[3 * s + 2] = e0;
+                // no proxy fence here: a consumer that wrote this stage's shared
+                // memory fenced itself before releasing it (a fence on this
+                // path would serialise the bulk copies)
                 unsigned char *base = smem + s * L::kStage;
                 const unsigned char *src_rp, *src_w, *src_u, *src_x, *src_xb, *src_c;
                 uint32_t brp, bw, b8 = 0, b4 = 0;
@@ -417,7 +510,9 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 aligned_span<8>(st.x, e0, cnt, &src_x, &b8);
                 aligned_span<8>(st.xbar, e0, cnt, &src_xb, &b8);
                 aligned_span<4>(mk.col, e0, cnt, &src_c, &b4);
-                mbar_expect_tx(&full[s], brp + bw + (cnt > 0 ? 3 * b8 + b4 : 0));
+                const unsigned char *src_tp = nullptr;
+                if (kScatter) aligned_span<4>(mk.tpos, e0, cnt, &src_tp, &b4);
+                mbar_expect_tx(&full[s], brp + bw + (cnt > 0 ? 3 * b8 + (kScatter ? 2 : 1) * b4 : 0));
                 bulk_g2s(base + L::kRp, src_rp, brp, &full[s]);
                 bulk_g2s(base + L::kW, src_w, bw, &full[s]);
                 if (cnt > 0) {
@@ -425,14 +520,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     bulk_g2s(base + L::kX, src_x, b8, &full[s]);
                     bulk_g2s_hint(base + L::kXB, src_xb, b8, &full[s], pol);
                     bulk_g2s_hint(base + L::kCol, src_c, b4, &full[s], pol);
+                    if (kScatter) bulk_g2s_hint(base + L::kTp, src_tp, b4, &full[s], pol);
                 }
             }
-            // drain: tiles still held by the other stages
-            for (int64_t jj = (j >= NSTAGE - 1 ? j - NSTAGE + 1 : 0); jj < j; ++jj) {
-                const int s = (int)(jj % NSTAGE);
-                mbar_wait(&empty[s], (uint32_t)((jj / NSTAGE) & 1));
-                finished(stile[s]);
-            }
+
         }
         return;
     }
@@ -446,10 +537,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             const int64_t k = stile[s];
             if (k >= 0) {
                 unsigned char *base = smem + s * L::kStage;
-                const int64_t r0 = mk.tiles[2 * k];
+                const int64_t r0 = smeta[3 * s];
                 const int lr = (int)(((r0 * 8) & 15) >> 3);
                 const int64_t *srp = reinterpret_cast<const int64_t *>(base + L::kRp) + lr;
-                const int nrows = (int)(mk.tiles[2 * k + 1] - r0);
+                const int nrows = (int)(smeta[3 * s + 1] - r0);
                 const int64_t e0 = srp[0];
                 const int cnt = (int)(srp[nrows] - e0);
                 const int d8 = (int)(((e0 * 8) & 15) >> 3), d4 = (int)(((e0 * 4) & 15) >> 2);
@@ -484,6 +575,154 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
 #ifdef MQ_NO_COLSUM  // timing experiment only: solver without column sums
     if (warp > NSW + NGW) return;
 #endif
+    if ((kScatter || kSplit) && warp > NSW + NGW) return;  // column sums run after the kernel
+#ifdef MQ_CS_PERWARP
+    if (warp > NSW + NGW) {  // ---------------------------------- column sums
+        // Each column-sum warp owns a contiguous range of goods and runs its
+        // own pipeline (no cross-warp barriers): per block, its slice of the
+        // schedule is contiguous in bperm and is staged in chunks with TMA
+        // (double-buffered, issued before the block is even solved); once
+        // every CTA has solved the block, the warp gathers a chunk's x values
+        // from L2 (kCsU independent loads per lane in flight) into shared
+        // memory, then each lane adds its goods' values in ascending row
+        // order (deterministic).
+        const int cw = warp - NSW - NGW - 1;
+        const int64_t per = (mk.m + gridDim.x - 1) / gridDim.x;
+        const int64_t c_lo = blockIdx.x * per;
+        const int64_t c_hi = c_lo + per < mk.m ? c_lo + per : mk.m;
+        const int64_t cn = c_hi > c_lo ? c_hi - c_lo : 0;
+        const int64_t wper = (cn + NCW - 1) / NCW;
+        const int64_t j_lo = c_lo + cw * wper;
+        const int64_t j_hi = j_lo + wper < c_hi ? j_lo + wper : c_hi;
+        const int nc = (int)(j_hi > j_lo ? j_hi - j_lo : 0);
+        // per-warp shared layout:
+        // sperm[2][kCsChunk+8] | sbptr[2][kWCols+8] | sval[kCsChunk] | meta[2][4] | cbar[2]
+        constexpr int kWarpStage = (2 * (kCsChunk + 8) + 2 * (kWCols + 8)) * 4 + kCsChunk * 8 +
+                                   8 * 8 + 2 * 8;
+        unsigned char *wbase = reinterpret_cast<unsigned char *>(cstage) +
+                               cw * ((kWarpStage + 127) / 128 * 128);
+        int32_t *sperm0 = reinterpret_cast<int32_t *>(wbase);
+        int32_t *sbptr0 = sperm0 + 2 * (kCsChunk + 8);
+        double *sval = reinterpret_cast<double *>(sbptr0 + 2 * (kWCols + 8));
+        int64_t *meta = reinterpret_cast<int64_t *>(sval + kCsChunk);
+        uint64_t *cbar = reinterpret_cast<uint64_t *>(meta + 8);
+        if (wl == 0) {
+            mbar_init(&cbar[0], 1);
+            mbar_init(&cbar[1], 1);
+            mbar_fence_init();
+        }
+        __syncwarp();
+        if (nc == 0) {  // no goods here: still publish progress for the throttle
+            if (wl == 0)
+                for (int64_t bb = 0; bb < mk.nblk; ++bb) atomicAdd(st.blk_done + mk.nblk + bb, 1);
+            return;
+        }
+        // staging cursor (lane 0 only)
+        int64_t g_stage = 0, sb = 0, sc0 = -1, srhi = 0;
+        auto stage_next = [&]() {
+            if (sb >= mk.nblk) return;
+            const int buf = (int)(g_stage & 1);
+            const bool first = sc0 < 0;
+            const int64_t row0 = sb * mk.m;
+            if (first) {
+                sc0 = __ldg(mk.bptr + row0 + j_lo);
+                srhi = __ldg(mk.bptr + row0 + j_hi);
+            }
+            const int64_t c1 = sc0 + kCsChunk < srhi ? sc0 + kCsChunk : srhi;
+            meta[4 * buf] = sc0;
+            meta[4 * buf + 1] = c1;
+            meta[4 * buf + 2] = srhi;
+            const unsigned char *srcp, *srcb;
+            uint32_t bp = 0, bb = 0;
+            if (c1 > sc0) aligned_span<4>(mk.bperm, sc0, c1 - sc0, &srcp, &bp);
+            if (first) aligned_span<4>(mk.bptr, row0 + j_lo, nc + 1, &srcb, &bb);
+            mbar_expect_tx(&cbar[buf], bp + bb);
+            if (c1 > sc0) bulk_g2s(sperm0 + buf * (kCsChunk + 8), srcp, bp, &cbar[buf]);
+            if (first) bulk_g2s(sbptr0 + (int)(sb & 1) * (kWCols + 8), srcb, bb, &cbar[buf]);
+            ++g_stage;
+            if (c1 >= srhi) {
+                ++sb;
+                sc0 = -1;
+            } else {
+                sc0 = c1;
+            }
+        };
+        double acc[QMAX];
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) acc[q] = 0.0;
+        if (wl == 0) {
+            stage_next();
+            stage_next();
+        }
+        int64_t g = 0;
+        for (int64_t blk = 0; blk < mk.nblk; ++blk) {
+            const int64_t kb0 = blk * tpb_all;
+            const int target = (int)((kb0 + tpb_all < mk.ntiles ? kb0 + tpb_all : mk.ntiles) - kb0);
+            {
+                MQ_T0();
+#ifndef MQ_CS_NOWAIT
+                if (wl == 0) wait_counter(st.blk_done + blk, target, st.faults, true);
+#endif
+                __syncwarp();
+                if (wl == 0) MQ_T1(3);
+            }
+            MQ_T0();
+            const int64_t row0 = blk * mk.m;
+            const int32_t *sbp = sbptr0 + (int)(blk & 1) * (kWCols + 8) +
+                                 (int)((((row0 + j_lo) * 4) & 15) >> 2);
+            for (;;) {
+                const int buf = (int)(g & 1);
+                mbar_wait(&cbar[buf], (uint32_t)((g >> 1) & 1));
+                const int64_t c0 = meta[4 * buf], c1 = meta[4 * buf + 1], rhi = meta[4 * buf + 2];
+                const int32_t *sp = sperm0 + buf * (kCsChunk + 8) + (int)(((c0 * 4) & 15) >> 2);
+                const int len = (int)(c1 - c0);
+                for (int t0 = wl; t0 < len; t0 += 32 * kCsU) {
+                    double v[kCsU];
+#pragma unroll
+                    for (int u = 0; u < kCsU; ++u) {
+                        const int t = t0 + u * 32;
+                        v[u] = t < len ? __ldcg(st.x + sp[t]) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kCsU; ++u) {
+                        const int t = t0 + u * 32;
+                        if (t < len) sval[t] = v[u];
+                    }
+                }
+                __syncwarp();  // values of the chunk are in shared memory
+#pragma unroll
+                for (int q = 0; q < QMAX; ++q) {
+                    const int jl = wl + q * 32;
+                    if (jl < nc) {
+                        int64_t lo = sbp[jl], hi = sbp[jl + 1];
+                        lo = lo > c0 ? lo : c0;
+                        hi = hi < c1 ? hi : c1;
+                        double a = acc[q];
+                        for (int64_t t = lo; t < hi; ++t) a += sval[t - c0];
+                        acc[q] = a;
+                    }
+                }
+                __syncwarp();  // chunk consumed: its buffers may be restaged
+                ++g;
+                if (wl == 0) stage_next();
+                if (c1 >= rhi) break;
+            }
+            if (wl == 0) {
+                MQ_T1(4);
+                atomicAdd(st.blk_done + mk.nblk + blk, 1);  // block gathered by this warp
+            }
+        }
+        if (write_cs) {
+#pragma unroll
+            for (int q = 0; q < QMAX; ++q) {
+                const int jl = wl + q * 32;
+                if (jl < nc) st.cs[j_lo + jl] = acc[q];
+            }
+        }
+        return;
+    }
+
+#else
     if (warp > NSW + NGW) {  // ---------------------------------- column sums
         // The CTA's NCW column-sum warps own goods [j_lo, j_hi); thread ct owns
         // j_lo + ct + q*NCW*32.  Per block, one thread stages the block's
@@ -607,9 +846,11 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         return;
     }
 
+#endif
     // ---------------------------------------------------------- solvers
     const int lane = tid & (G - 1);
     const int gsub = wl / G;
+    const uint64_t pkeep = policy_evict_last();
     const Avg av = avg_weights(st.navg, it);
     int64_t my_sweeps = 0;
     int64_t my_faults = 0;
@@ -627,15 +868,15 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         const int64_t blk = k / tpb_all;
         {
             MQ_T0();
-#ifndef MQ_NO_COLSUM
-            if (blk >= kLag && wl == 0)
-                wait_counter(st.blk_done + mk.nblk + (blk - kLag), (int)gridDim.x, st.faults,
-                             false);
+#if !defined(MQ_NO_COLSUM) && !defined(MQ_CS_NOWAIT)
+            if (!kScatter && !kSplit && blk >= kLag && wl == 0)
+                wait_counter(st.blk_done + mk.nblk + (blk - kLag),
+                             (int)gridDim.x * (kCsPerWarp ? NCW : 1), st.faults, false);
 #endif
             __syncwarp();
             if (wl == 0) MQ_T1(1);
         }
-        const int64_t r0 = mk.tiles[2 * k], r1 = mk.tiles[2 * k + 1];
+        const int64_t r0 = smeta[3 * s], r1 = smeta[3 * s + 1];
         const int nrows = (int)(r1 - r0);
         unsigned char *base = smem + s * L::kStage;
         const int lr = (int)(((r0 * 8) & 15) >> 3);
@@ -650,6 +891,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         // written over x in place for the shared-memory path)
         double *sc = reinterpret_cast<double *>(base + (NGW > 0 ? L::kC : L::kX)) + d8;
         const int32_t *scol = reinterpret_cast<const int32_t *>(base + L::kCol) + d4;
+        const int32_t *stp = reinterpret_cast<const int32_t *>(base + L::kTp) + d4;
 
         for (;;) {
             int rb = 0;
@@ -667,7 +909,19 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             }
             int nsw = 0;
             bool ok = true;
+#ifdef MQ_TRIVIAL_SOLVE  // bandwidth experiment: stream the tile, skip the solve
+            if (MQ_TRIVIAL_SOLVE == 1) {
+                for (int t = a + lane; t < b; t += G) {
+                    const double xn = sx[t] + 1e-300 * su[t];
+                    st.x[e0 + t] = xn;
+                    __stcs(st.xbar + e0 + t, av.wold * sxb[t] + av.wnew * xn);
+                    if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
+                }
+            }
+            if (false) {
+#else
             if (kRegPer > 0 && __all_sync(MQ_FULL, b - a <= kRegPer * G)) {
+#endif
                 // ---- row in registers
                 constexpr int RP = kRegPer > 0 ? kRegPer : 1;
                 double c[RP], u[RP];
@@ -707,9 +961,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                         const double xn = fmax(c[e] + tw * u[e] * inv_s, 0.0);
                         st.x[e0 + t] = xn;
                         __stcs(st.xbar + e0 + t, av.wold * sxb[t] + av.wnew * xn);
+                        if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
                     }
                 }
-            } else {
+            } else if (!kTrivial) {
                 // ---- longer rows: stream the row from shared memory
                 double s0p = 0.0, ap = 0.0, bp = 0.0;
                 for (int t = a + lane; t < b; t += G) {
@@ -736,7 +991,11 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     const double xn = fmax(sc[t] + tw * su[t] * inv_s, 0.0);
                     st.x[e0 + t] = xn;
                     __stcs(st.xbar + e0 + t, av.wold * sxb[t] + av.wnew * xn);
+                    if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
                 }
+                // c was written over x in this stage: order those generic-proxy
+                // writes before the producer's next bulk copy into the stage
+                if (NGW == 0) fence_proxy_async();
             }
             if (has && b > a && lane == 0) {
                 my_sweeps += nsw;
@@ -744,7 +1003,20 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             }
         }
         __syncwarp();
-        if (wl == 0) mbar_arrive(&empty[s]);
+        if (wl == 0) {
+            // the last solver warp out of the tile publishes it (one gpu-scope
+            // fence per tile, off the producer's path)
+            int prior;
+            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                         : "=r"(prior) : "r"(smem_addr(&claim[NSTAGE + s])) : "memory");
+#ifndef MQ_NO_PUBLISH
+            if (!kSplit && !kScatter && prior == NSW - 1) {
+                __threadfence();
+                atomicAdd(&st.blk_done[k / tpb_all], 1);
+            }
+#endif
+            mbar_arrive(&empty[s]);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -858,6 +1130,7 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
             const double xn = fmax(xe - tau * st.p[mk.col[t]] + tw * mk.u[t] * inv_s, 0.0);
             st.x[t] = xn;
             st.xbar[t] = av.wold * st.xbar[t] + av.wnew * xn;
+            if (kScatter) st.xc[mk.tpos[t]] = xn;
         }
         __syncthreads();
     }
@@ -900,6 +1173,70 @@ colsum_blocks_kernel(int64_t m, const int32_t *__restrict__ bptr, const int32_t 
     }
 }
 
+// Scatter mode: xc holds x in column-major order, so a good's entries are
+// contiguous: one warp per good streams them (coalesced, 4 loads in flight
+// per lane, fixed butterfly => deterministic).
+__global__ void __launch_bounds__(256)
+colsum_xc_kernel(int64_t m, const int64_t *__restrict__ tptr, const double *__restrict__ xc,
+                 double *__restrict__ out, double *__restrict__ csbar,
+                 const int64_t *__restrict__ navg, int it) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    Avg av = {0.0, 0.0};
+    if (csbar) av = avg_weights(navg, it);
+    for (int64_t j = warp_id; j < m; j += nwarps) {
+        const int64_t beg = tptr[j], end = tptr[j + 1];
+        double acc = 0.0;
+        int64_t t = beg + lane;
+        for (; t + 96 < end; t += 128) {
+            const double v0 = __ldcs(xc + t), v1 = __ldcs(xc + t + 32);
+            const double v2 = __ldcs(xc + t + 64), v3 = __ldcs(xc + t + 96);
+            acc += v0;
+            acc += v1;
+            acc += v2;
+            acc += v3;
+        }
+        for (; t < end; t += 32) acc += __ldcs(xc + t);
+        acc = group_sum<32>(acc);
+        if (lane == 0) {
+            out[j] = acc;
+            if (csbar) csbar[j] = av.wold * csbar[j] + av.wnew * acc;
+        }
+    }
+}
+
+// Split mode: column sums of one block of tiles right after its primal
+// launch, while its x is L2-resident: one warp per good, lanes stride the
+// good's segment (coalesced bperm, independent gathers), fixed butterfly;
+// blocks are added into cs in order (deterministic).
+__global__ void __launch_bounds__(256)
+colsum_seg_kernel(int64_t m, const int32_t *__restrict__ bptr, const int32_t *__restrict__ bperm,
+                  int64_t b, const double *__restrict__ x, double *__restrict__ cs) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t row0 = b * m;
+    for (int64_t j = warp_id; j < m; j += nwarps) {
+        const int64_t beg = bptr[row0 + j], end = bptr[row0 + j + 1];
+        double acc = 0.0;
+        int64_t t = beg + lane;
+        for (; t + 96 < end; t += 128) {
+            const int32_t k0 = __ldcs(bperm + t), k1 = __ldcs(bperm + t + 32);
+            const int32_t k2 = __ldcs(bperm + t + 64), k3 = __ldcs(bperm + t + 96);
+            const double v0 = __ldcg(x + k0), v1 = __ldcg(x + k1);
+            const double v2 = __ldcg(x + k2), v3 = __ldcg(x + k3);
+            acc += v0;
+            acc += v1;
+            acc += v2;
+            acc += v3;
+        }
+        for (; t < end; t += 32) acc += __ldcg(x + __ldcs(bperm + t));
+        acc = group_sum<32>(acc);
+        if (lane == 0) cs[j] = b == 0 ? acc : cs[j] + acc;
+    }
+}
+
 __global__ void colsum_finalize_kernel(int64_t m, const double *__restrict__ cs,
                                        double *__restrict__ csbar, const int64_t *__restrict__ navg,
                                        int it) {
@@ -923,31 +1260,24 @@ static int sm_count() {
     return n;
 }
 
-#ifndef MQ_G
-#define MQ_G 16
-#endif
-#ifndef MQ_NCW
-#define MQ_NCW 4
-#endif
-#ifndef MQ_NSW
-#define MQ_NSW 15
-#endif
-#ifndef MQ_NGW
-#define MQ_NGW 0
-#endif
-#ifndef MQ_ETILE
-#define MQ_ETILE MQ_TILE_ENTRIES
-#endif
-#ifndef MQ_STAGES
-#define MQ_STAGES 3
-#endif
 constexpr int kG = MQ_G, kNSW = MQ_NSW, kNGW = MQ_NGW, kNCW = MQ_NCW, kStages = MQ_STAGES;
 constexpr int kEtile = MQ_ETILE;
-constexpr int kQMax = (1152 + kNCW * 32 - 1) / (kNCW * 32);
+#ifdef MQ_CS_PERWARP
+constexpr int kQMax = (kWCols + 31) / 32;  // goods per column-sum lane
+#else
+constexpr int kQMax = (1152 + kNCW * 32 - 1) / (kNCW * 32);  // goods per column-sum thread
+#endif
 using PrimalLayout = TileLayout<kEtile, MQ_TILE_ROWS, (kNGW > 0)>;
-static_assert(kQMax * kNCW * 32 >= kCsCols, "column-sum threads cannot cover a slice");
-constexpr int kPrimalSmem = kStages * PrimalLayout::kStage + 4 * kStages * 8 + 4 * kStages * 4 + 128 +
-                            (kCsCap + kCsCols + 8) * 4 + 4 * 8 + 16;
+
+constexpr int kPrimalSmem = kStages * PrimalLayout::kStage + 7 * kStages * 8 + 4 * kStages * 4 + 128 +
+                            ((kScatter || kSplit) ? 0 :
+#ifdef MQ_CS_PERWARP
+                             kNCW * (((2 * (kCsChunk + 8) + 2 * (kWCols + 8)) * 4 + kCsChunk * 8 +
+                                      8 * 8 + 2 * 8 + 127) / 128 * 128)
+#else
+                             (kCsCap + kCsCols + 8) * 4 + 4 * 8 + 16
+#endif
+                            );
 
 int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev, cudaStream_t s) {
     static bool configured = false;
@@ -958,12 +1288,26 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
         if (e != cudaSuccess) return set_error(e, "mq_primal_step: smem attribute");
         configured = true;
     }
-    if (mk->ntiles > 0) {
+    const int nthr = (kNSW + kNGW + kNCW + 1) * 32;
+    if (mk->ntiles > 0 && kSplit) {
+        // per block of tiles: the primal sweep, then the block's column sums
+        // while its x is still in L2
+        cudaMemsetAsync(st->blk_done, 0, sizeof(int32_t) * ((size_t)mk->nblk + 1), s);
+        const int cgrid = grid_for(mk->m, 8, sm_count() * 8);
+        for (int64_t b = 0; b < mk->nblk; ++b) {
+            const int64_t lo = b * mk->tiles_per_block;
+            const int64_t hi = lo + mk->tiles_per_block < mk->ntiles ? lo + mk->tiles_per_block
+                                                                     : mk->ntiles;
+            const int grid = (int)(hi - lo < mk->prim_grid ? hi - lo : mk->prim_grid);
+            kern<<<grid, nthr, kPrimalSmem, s>>>(*mk, *st, it, xprev, 0, lo, hi, st->blk_done + b);
+            colsum_seg_kernel<<<cgrid, 256, 0, s>>>(mk->m, mk->bptr, mk->bperm, b, st->x, st->cs);
+        }
+    } else if (mk->ntiles > 0) {
         if ((mk->m + mk->prim_grid - 1) / mk->prim_grid > (int64_t)kCsCols)
             return set_error(cudaErrorInvalidValue, "mq_primal_step: too many goods per CTA");
         cudaMemsetAsync(st->blk_done, 0, sizeof(int32_t) * (2 * (size_t)mk->nblk + 1), s);
-        kern<<<mk->prim_grid, (kNSW + kNGW + kNCW + 1) * 32, kPrimalSmem, s>>>(*mk, *st, it,
-                                                                                xprev, 1);
+        kern<<<mk->prim_grid, nthr, kPrimalSmem, s>>>(*mk, *st, it, xprev, 1, 0, mk->ntiles,
+                                                      st->blk_done + 2 * mk->nblk);
     } else {
         cudaMemsetAsync(st->cs, 0, sizeof(double) * (size_t)mk->m, s);
     }
@@ -977,6 +1321,11 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
 // adds the long rows (pseudo-block nblk) to cs; csbar update when finalize
 int colsum_rest_launch(const mq_market *mk, const mq_state *st, int it, int finalize,
                        cudaStream_t s) {
+    if (kScatter) {
+        colsum_xc_kernel<<<grid_for(mk->m, 8, sm_count() * 8), 256, 0, s>>>(
+            mk->m, mk->tptr, st->xc, st->cs, finalize ? st->csbar : nullptr, st->navg, it);
+        return check_launch("mq_colsum_step");
+    }
     const int grid = (int)((mk->m + 255) / 256);
     if (mk->nlong > 0) {
         colsum_blocks_kernel<<<grid, 256, 0, s>>>(mk->m, mk->bptr, mk->bperm, mk->nblk,
@@ -1049,6 +1398,8 @@ int mq_debug_counters(unsigned long long *out_host) {
 }
 
 int mq_tile_entries(void) { return kEtile; }
+
+int mq_colsum_mode(void) { return kScatter ? 1 : (kSplit ? 2 : 0); }
 
 int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream) {
     const int grid = (int)((mk->m + 255) / 256);

@@ -3,7 +3,7 @@
     row_ptr  int64 [n+1 (+pad)]   w       float64 [n (+pad)]   scales float64 [n]
     col      int32 [nnz (+pad)]   u       float64 [nnz (+pad)] (row max 1)
     u_orig   float64 [nnz]        (residuals are measured on the original data)
-    tiles    int64 [ntiles, 2]    row ranges of <= 2048 entries / 256 rows
+    tiles    int64 [ntiles, 4]    (r0, r1, e0, e1): rows / entries of each tile
     long_rows int32 [nlong]       rows longer than 1024 entries
     bperm    int32 [nnz]          tile-blocked transpose schedule: per block of
     bptr     int32 [(nblk+1)m+1]  8 x prim_grid tiles, per good, ascending rows
@@ -85,19 +85,39 @@ def build_tiles(row_ptr, tile_entries=nat.TILE_ENTRIES, long_row=nat.LONG_ROW,
 TILES_PER_CTA_PER_BLOCK = 4
 
 
+def build_transpose(col, m):
+    """(tpos int32 [nnz + pad], tptr int64 [m+1]): column-major position of
+    every entry under the stable column grouping of sparse.py:130-145."""
+    dev = col.device
+    nnz = col.numel()
+    tpos = torch.zeros(nnz + nat.PAD, dtype=torch.int32, device=dev)
+    if nnz:
+        _, perm = torch.sort(col, stable=True)
+        tpos[:nnz].scatter_(0, perm, torch.arange(nnz, dtype=torch.int32, device=dev))
+        del perm
+    counts = (torch.bincount(col.to(torch.int64), minlength=m) if nnz
+              else torch.zeros(m, dtype=torch.int64, device=dev))
+    tptr = torch.zeros(m + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(counts, 0, out=tptr[1:])
+    return tpos, tptr
+
+
 def sm_count(device):
     return torch.cuda.get_device_properties(device).multi_processor_count
 
 
+SPLIT_TILES_PER_BLOCK = 2048   # colsum mode 2: ~4M entries (32 MB of x) per block
+
+
 def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
-                           tiles_per_cta=TILES_PER_CTA_PER_BLOCK):
+                           tiles_per_cta=TILES_PER_CTA_PER_BLOCK, tiles_per_block=None):
     """Entry positions grouped by (block of tiles, good), ascending inside a
     good; long-row entries form the last pseudo-block.  Returns
     (bperm int32 [nnz], bptr int32 [(nblk+1)*m+1], nblk, tiles_per_block)."""
     dev = col.device
     nnz = col.numel()
     ntiles = int(tiles.shape[0])
-    tpb = max(1, tiles_per_cta * max(1, prim_grid))
+    tpb = tiles_per_block or max(1, tiles_per_cta * max(1, prim_grid))
     nblk = -(-ntiles // tpb)
     pos = torch.arange(nnz, device=dev, dtype=torch.int64)
     if nblk:
@@ -182,14 +202,23 @@ class DeviceMarket:
                                if self.nnz else torch.zeros(self.m, dtype=torch.int64,
                                                             device=dev))
             etile = int(self.lib.mq_tile_entries())
-            self.tiles, self.long_rows = build_tiles(self.row_ptr, etile,
-                                                     min(nat.LONG_ROW, etile // 2))
+            tiles2, self.long_rows = build_tiles(self.row_ptr, etile,
+                                                 min(nat.LONG_ROW, etile // 2))
+            # (r0, r1, e0, e1) per tile: the producer warp needs no dependent loads
+            self.tiles = torch.cat([tiles2, self.row_ptr[tiles2]], 1).contiguous()
             self.prim_grid = int(min(max(1, self.tiles.shape[0]), sm_count(dev)))
+            mode = int(self.lib.mq_colsum_mode())
             self.bperm, self.bptr, self.nblk, self.tiles_per_block = build_blocked_schedule(
-                self.row_ptr, self.col, self.m, self.tiles, self.long_rows, self.prim_grid)
+                self.row_ptr, self.col, self.m, tiles2, self.long_rows, self.prim_grid,
+                tiles_per_block=SPLIT_TILES_PER_BLOCK if mode == 2 else None)
             lens = self.row_ptr[1:] - self.row_ptr[:-1]
             self.max_row_len = int(lens.max().item()) if self.n else 0
         self.tperm = self.tptr = None
+        self.colsum_mode = int(self.lib.mq_colsum_mode())
+        self._tpos = self._tptr_c = None
+        if self.colsum_mode == 1:
+            with torch.cuda.device(dev):
+                self._tpos, self._tptr_c = build_transpose(self.col, self.m)
         self.struct = self._make_struct()
 
     def global_schedule(self):
@@ -220,6 +249,9 @@ class DeviceMarket:
         s.nblk = int(self.nblk)
         s.tiles_per_block = int(self.tiles_per_block)
         s.prim_grid = int(self.prim_grid)
+        if self._tpos is not None:
+            s.tpos = self._tpos.data_ptr()
+            s.tptr = self._tptr_c.data_ptr()
         s.row_begin = self.row_begin
         return s
 

@@ -132,6 +132,8 @@ class PdhcgEngine:
         self.x0 = torch.zeros(nnz, **f64)
         # per block: tiles solved, then column-sum warps done (throttle)
         self.blk_done = torch.zeros(2 * dm.nblk + 1, dtype=torch.int32, device=dev)
+        # column-major copy of x (only for a scatter-mode build)
+        self.xc = torch.zeros(nnz if getattr(dm, "colsum_mode", 0) == 1 else 1, **f64)
         self.p = torch.zeros(m, **f64)
         self.pbar = torch.zeros(m, **f64)
         self.p0 = torch.zeros(m, **f64)
@@ -162,8 +164,8 @@ class PdhcgEngine:
         if not isinstance(self.ops, NativeOps):
             return None
         s = nat.MqState()
-        for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "blk_done", "steps",
-                     "faults"):
+        for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "blk_done", "xc",
+                     "steps", "faults"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.navg = self.navg_dev.data_ptr()
         s.pass_out = self.pass_buf.data_ptr()

@@ -173,14 +173,18 @@ def test_abi_marshaling_without_device():
         "mq_normalize_rows": (0, None, None, None, None, None),
         "mq_gen_degrees": (0, 1, 10, 0, 0.5, 2.0, 1.0, 1, None, None),
         "mq_tile_entries": (),
+        "mq_colsum_mode": (),
         "mq_gen_fill": (0, 1, 10, 0, 0.5, 2.0, 1.0, 1, None, None, None, None, None),
         "mq_pdhcg_chunk": (0, 0, None, None, None, None, None, None, None, None, None, None,
                            None, 0, 0.1, 0.1, 32, 1e-10, 1, None, None, ctypes.byref(n64), None),
     }
     for name, args in calls.items():
         rc = getattr(lib, name)(*args)
+        if name == "mq_colsum_mode":
+            assert rc in (0, 1, 2)
+            continue
         assert rc != 0, name
-        if name == "mq_tile_entries":
+        if name in ("mq_tile_entries", "mq_colsum_mode"):
             continue
         assert lib.mq_last_error()
 

@@ -32,7 +32,7 @@ nsm = dm.prim_grid
 names = ["solver wait tile", "solver throttled", "producer wait stage", "colsum wait block",
          "colsum gather", "solver pass1", "solver root", "solver write"]
 print(f"{cfg}: {ms:.3f} ms/iter, kernel-cycles/SM ~{cyc:.3e}")
-per_warp = {0: 16, 1: 16, 2: 1, 3: 1, 4: 1, 5: 16, 6: 16, 7: 16}
+per_warp = {0: 15, 1: 15, 2: 1, 3: 4, 4: 4, 5: 15, 6: 15, 7: 15}
 for i, nm in enumerate(names):
     v = buf[i] / 10 / nsm / per_warp[i]
     print(f"  {nm:22s} {v:.3e} cycles per warp per iter ({100 * v / cyc:.1f}% of iter)")
