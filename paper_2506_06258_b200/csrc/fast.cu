@@ -300,8 +300,14 @@ constexpr bool kScatter = false;
 #ifdef MQ_COLSUM_SPLIT
 constexpr bool kSplit = !kScatter;    // per block of tiles: primal launch, then gather launch
 #else
-constexpr bool kSplit = false;        // column sums gathered in-kernel (column-sum warps)
+constexpr bool kSplit = false;
 #endif
+#if defined(MQ_COLSUM_PHASED) && !defined(MQ_COLSUM_SPLIT) && !defined(MQ_SCATTER)
+constexpr bool kPhased = true;        // solve a block of tiles, grid barrier, gather it from L2
+#else
+constexpr bool kPhased = false;       // default: column-sum warps gather concurrently (fused)
+#endif
+constexpr int kPhChunk = 4096;        // gathered values staged per round (phased mode)
 
 template <int ETILE, int RTILE, bool HASC>
 struct TileLayout {
@@ -410,6 +416,71 @@ __device__ __forceinline__ void wait_counter(const int *ctr, int target, int64_t
     if (acquire) __threadfence();
 }
 
+
+// ---- phased column sums -------------------------------------------------
+// Participants: the NSW solver warps and the NCW column-sum warps of the CTA
+// (pt = 0..NP-1).  After every CTA has solved block b (grid barrier), the
+// participants gather the block's x values of the CTA's goods from L2 into
+// shared memory in chunks (independent loads), then each thread adds its
+// goods' values in ascending row order (deterministic).
+__device__ __forceinline__ void phase_sync(int np) {
+    asm volatile("bar.sync 1, %0;" ::"r"(np) : "memory");
+}
+
+template <int QM>
+__device__ __forceinline__ void phased_gather(const mq_market &mk, const mq_state &st, int64_t b,
+                                              int pt, int np, int64_t j_lo, int nc,
+                                              double *sval, double (&acc)[QM]) {
+    phase_sync(np);  // this CTA has solved all its tiles of block b
+    if (pt == 0) {
+        int *gb = st.blk_done + mk.nblk + b;
+        __threadfence();
+        atomicAdd(gb, 1);
+        wait_counter(gb, (int)gridDim.x, st.faults, true);
+    }
+    phase_sync(np);  // every CTA has: block b's x is complete
+    if (nc == 0) return;
+    const int64_t row0 = b * mk.m;
+    const int64_t r_lo = __ldg(mk.bptr + row0 + j_lo), r_hi = __ldg(mk.bptr + row0 + j_lo + nc);
+    int32_t lo[QM], hi[QM];
+#pragma unroll
+    for (int q = 0; q < QM; ++q) {
+        const int jl = pt + q * np;
+        lo[q] = hi[q] = 0;
+        if (jl < nc) {
+            lo[q] = __ldg(mk.bptr + row0 + j_lo + jl);
+            hi[q] = __ldg(mk.bptr + row0 + j_lo + jl + 1);
+        }
+    }
+    for (int64_t c0 = r_lo; c0 < r_hi; c0 += kPhChunk) {
+        const int len = (int)(r_hi - c0 < kPhChunk ? r_hi - c0 : kPhChunk);
+        for (int t0 = pt; t0 < len; t0 += np * 4) {
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = t0 + u * np;
+                v[u] = t < len ? __ldcg(st.x + __ldcs(mk.bperm + c0 + t)) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = t0 + u * np;
+                if (t < len) sval[t] = v[u];
+            }
+        }
+        phase_sync(np);
+        const int64_t c1 = c0 + len;
+#pragma unroll
+        for (int q = 0; q < QM; ++q) {
+            int64_t t = lo[q] > c0 ? lo[q] : c0;
+            const int64_t e = hi[q] < c1 ? hi[q] : c1;
+            double a = acc[q];
+            for (; t < e; ++t) a += sval[t - c0];
+            acc[q] = a;
+        }
+        phase_sync(np);
+    }
+}
+
 // Warps 0..NSW-1 solve rows, warp NSW produces (TMA), warps NSW+1..NSW+NGW
 // gather prices (c = x - tau p[col] for the whole tile), the last NCW warps
 // sum columns.  full[s]: stage s has landed; ready[s]: its c is computed;
@@ -449,6 +520,69 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
     if (warp == NSW) {  // ---------------------------------------- producer
         if (wl == 0) {
             const uint64_t pol = policy_evict_first();
+            if (kPhased) {
+                // blocks of tiles one after the other; within a block tiles are
+                // claimed dynamically; a marker stage (-2) ends each block
+                int64_t j = 0;
+                for (int64_t bk = 0; bk <= mk.nblk; ++bk) {
+                    const bool last = bk == mk.nblk;
+                    const int64_t lo = bk * tpb_all;
+                    const int64_t hi = last ? lo : (lo + tpb_all < mk.ntiles ? lo + tpb_all : mk.ntiles);
+                    int *ctr = st.blk_done + (last ? 0 : bk);
+                    int64_t batch = last ? hi : lo + atomicAdd(ctr, kClaim);
+                    int bpos = 0;
+                    for (;;) {
+                        int64_t k = hi;
+                        if (!last) {
+                            if (bpos == kClaim) {
+                                batch = lo + atomicAdd(ctr, kClaim);
+                                bpos = 0;
+                            }
+                            k = batch + bpos++;
+                        }
+                        longlong2 m01 = {0, 0}, m23 = {0, 0};
+                        if (k < hi) {
+                            const longlong2 *tp = reinterpret_cast<const longlong2 *>(mk.tiles + 4 * k);
+                            m01 = __ldg(tp);
+                            m23 = __ldg(tp + 1);
+                        }
+                        const int s = (int)(j % NSTAGE);
+                        if (j >= NSTAGE) mbar_wait(&empty[s], (uint32_t)(((j / NSTAGE) - 1) & 1));
+                        ++j;
+                        claim[s] = 0;
+                        claim[NSTAGE + s] = 0;
+                        if (k >= hi) {  // end of block (-2) or of the launch (-1)
+                            stile[s] = last ? -1 : -2;
+                            mbar_expect_tx(&full[s], 0);
+                            break;
+                        }
+                        const int64_t r0 = m01.x, r1 = m01.y, e0 = m23.x, cnt = m23.y - m23.x;
+                        stile[s] = k;
+                        smeta[3 * s] = r0;
+                        smeta[3 * s + 1] = r1;
+                        smeta[3 * s + 2] = e0;
+                        unsigned char *base = smem + s * L::kStage;
+                        const unsigned char *src_rp, *src_w, *src_u, *src_x, *src_xb, *src_c;
+                        uint32_t brp, bw, b8 = 0, b4 = 0;
+                        aligned_span<8>(mk.row_ptr, r0, r1 - r0 + 1, &src_rp, &brp);
+                        aligned_span<8>(mk.w, r0, r1 - r0, &src_w, &bw);
+                        aligned_span<8>(mk.u, e0, cnt, &src_u, &b8);
+                        aligned_span<8>(st.x, e0, cnt, &src_x, &b8);
+                        aligned_span<8>(st.xbar, e0, cnt, &src_xb, &b8);
+                        aligned_span<4>(mk.col, e0, cnt, &src_c, &b4);
+                        mbar_expect_tx(&full[s], brp + bw + (cnt > 0 ? 3 * b8 + b4 : 0));
+                        bulk_g2s(base + L::kRp, src_rp, brp, &full[s]);
+                        bulk_g2s(base + L::kW, src_w, bw, &full[s]);
+                        if (cnt > 0) {
+                            bulk_g2s_hint(base + L::kU, src_u, b8, &full[s], pol);
+                            bulk_g2s(base + L::kX, src_x, b8, &full[s]);
+                            bulk_g2s_hint(base + L::kXB, src_xb, b8, &full[s], pol);
+                            bulk_g2s_hint(base + L::kCol, src_c, b4, &full[s], pol);
+                        }
+                    }
+                }
+                return;
+            }
             // tiles are claimed dynamically (global counter, kClaim at a time) so
             // that every block of tiles completes with little skew across CTAs;
             // the next tile's claim and metadata are fetched one step ahead so
@@ -576,6 +710,29 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
     if (warp > NSW + NGW) return;
 #endif
     if ((kScatter || kSplit) && warp > NSW + NGW) return;  // column sums run after the kernel
+    // phased mode: goods of this CTA and the participant layout
+    constexpr int NP = (NSW + NCW) * 32;
+    constexpr int PQ = 2048 / NP + 1;  // goods per participant (<= 2048 goods per CTA)
+    const int64_t ph_per = (mk.m + gridDim.x - 1) / gridDim.x;
+    const int64_t ph_lo = blockIdx.x * ph_per;
+    const int ph_nc = (int)(ph_lo + ph_per < mk.m ? ph_per : (mk.m > ph_lo ? mk.m - ph_lo : 0));
+    double *ph_sval = reinterpret_cast<double *>(cstage);
+    double ph_acc[PQ];
+#pragma unroll
+    for (int q = 0; q < PQ; ++q) ph_acc[q] = 0.0;
+    if (kPhased && warp > NSW + NGW) {  // column-sum warps: gather phases only
+        const int pt = tid - 32 * (1 + NGW);
+        for (int64_t bk = 0; bk < mk.nblk; ++bk)
+            phased_gather<PQ>(mk, st, bk, pt, NP, ph_lo, ph_nc, ph_sval, ph_acc);
+        if (write_cs) {
+#pragma unroll
+            for (int q = 0; q < PQ; ++q) {
+                const int jl = pt + q * NP;
+                if (jl < ph_nc) st.cs[ph_lo + jl] = ph_acc[q];
+            }
+        }
+        return;
+    }
 #ifdef MQ_CS_PERWARP
     if (warp > NSW + NGW) {  // ---------------------------------- column sums
         // Each column-sum warp owns a contiguous range of goods and runs its
@@ -854,6 +1011,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
     const Avg av = avg_weights(st.navg, it);
     int64_t my_sweeps = 0;
     int64_t my_faults = 0;
+    int64_t ph_blk = 0;
     for (int64_t j = 0;; ++j) {
         const int s = (int)(j % NSTAGE);
         {
@@ -862,6 +1020,13 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             if (wl == 0) MQ_T1(0);
         }
         const int64_t k = stile[s];
+        if (kPhased && k == -2) {  // end of a block: release the stage, then gather
+            __syncwarp();
+            if (wl == 0) mbar_arrive(&empty[s]);
+            phased_gather<PQ>(mk, st, ph_blk, tid, NP, ph_lo, ph_nc, ph_sval, ph_acc);
+            ++ph_blk;
+            continue;
+        }
         if (k < 0) break;  // sentinel
         // throttle: stay within kLag blocks of the column-sum front, so the
         // blocks still to be gathered are L2-resident
@@ -869,7 +1034,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         {
             MQ_T0();
 #if !defined(MQ_NO_COLSUM) && !defined(MQ_CS_NOWAIT)
-            if (!kScatter && !kSplit && blk >= kLag && wl == 0)
+            if (!kScatter && !kSplit && !kPhased && blk >= kLag && wl == 0)
                 wait_counter(st.blk_done + mk.nblk + (blk - kLag),
                              (int)gridDim.x * (kCsPerWarp ? NCW : 1), st.faults, false);
 #endif
@@ -1010,12 +1175,19 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                          : "=r"(prior) : "r"(smem_addr(&claim[NSTAGE + s])) : "memory");
 #ifndef MQ_NO_PUBLISH
-            if (!kSplit && !kScatter && prior == NSW - 1) {
+            if (!kSplit && !kScatter && !kPhased && prior == NSW - 1) {
                 __threadfence();
                 atomicAdd(&st.blk_done[k / tpb_all], 1);
             }
 #endif
             mbar_arrive(&empty[s]);
+        }
+    }
+    if (kPhased && write_cs) {
+#pragma unroll
+        for (int q = 0; q < PQ; ++q) {
+            const int jl = tid + q * NP;
+            if (jl < ph_nc) st.cs[ph_lo + jl] = ph_acc[q];
         }
     }
 #pragma unroll
@@ -1270,7 +1442,7 @@ constexpr int kQMax = (1152 + kNCW * 32 - 1) / (kNCW * 32);  // goods per column
 using PrimalLayout = TileLayout<kEtile, MQ_TILE_ROWS, (kNGW > 0)>;
 
 constexpr int kPrimalSmem = kStages * PrimalLayout::kStage + 7 * kStages * 8 + 4 * kStages * 4 + 128 +
-                            ((kScatter || kSplit) ? 0 :
+                            (kPhased ? kPhChunk * 8 : (kScatter || kSplit) ? 0 :
 #ifdef MQ_CS_PERWARP
                              kNCW * (((2 * (kCsChunk + 8) + 2 * (kWCols + 8)) * 4 + kCsChunk * 8 +
                                       8 * 8 + 2 * 8 + 127) / 128 * 128)
@@ -1302,6 +1474,12 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
             kern<<<grid, nthr, kPrimalSmem, s>>>(*mk, *st, it, xprev, 0, lo, hi, st->blk_done + b);
             colsum_seg_kernel<<<cgrid, 256, 0, s>>>(mk->m, mk->bptr, mk->bperm, b, st->x, st->cs);
         }
+    } else if (mk->ntiles > 0 && kPhased) {
+        if ((mk->m + mk->prim_grid - 1) / mk->prim_grid > 2048)
+            return set_error(cudaErrorInvalidValue, "mq_primal_step: too many goods per CTA");
+        cudaMemsetAsync(st->blk_done, 0, sizeof(int32_t) * (2 * (size_t)mk->nblk + 1), s);
+        kern<<<mk->prim_grid, nthr, kPrimalSmem, s>>>(*mk, *st, it, xprev, 1, 0, mk->ntiles,
+                                                      st->blk_done);
     } else if (mk->ntiles > 0) {
         if ((mk->m + mk->prim_grid - 1) / mk->prim_grid > (int64_t)kCsCols)
             return set_error(cudaErrorInvalidValue, "mq_primal_step: too many goods per CTA");
@@ -1399,7 +1577,7 @@ int mq_debug_counters(unsigned long long *out_host) {
 
 int mq_tile_entries(void) { return kEtile; }
 
-int mq_colsum_mode(void) { return kScatter ? 1 : (kSplit ? 2 : 0); }
+int mq_colsum_mode(void) { return kScatter ? 1 : (kSplit ? 2 : (kPhased ? 3 : 0)); }
 
 int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream) {
     const int grid = (int)((mk->m + 255) / 256);

@@ -106,7 +106,7 @@ def sm_count(device):
     return torch.cuda.get_device_properties(device).multi_processor_count
 
 
-SPLIT_TILES_PER_BLOCK = 2048   # colsum mode 2: ~4M entries (32 MB of x) per block
+SPLIT_TILES_PER_BLOCK = 2048   # colsum modes 2/3: ~4M entries (32 MB of x) per block
 
 
 def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
@@ -210,7 +210,7 @@ class DeviceMarket:
             mode = int(self.lib.mq_colsum_mode())
             self.bperm, self.bptr, self.nblk, self.tiles_per_block = build_blocked_schedule(
                 self.row_ptr, self.col, self.m, tiles2, self.long_rows, self.prim_grid,
-                tiles_per_block=SPLIT_TILES_PER_BLOCK if mode == 2 else None)
+                tiles_per_block=SPLIT_TILES_PER_BLOCK if mode in (2, 3) else None)
             lens = self.row_ptr[1:] - self.row_ptr[:-1]
             self.max_row_len = int(lens.max().item()) if self.n else 0
         self.tperm = self.tptr = None

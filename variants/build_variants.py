@@ -4,10 +4,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2506_06258_b200 import _build
 HERE = os.path.dirname(os.path.abspath(__file__))
 V = {
-  "cta": dict(),
-  "perwarp": dict(MQ_CS_PERWARP=1),
-  "cta_b": dict(),
-  "perwarp_b": dict(MQ_CS_PERWARP=1),
+  "phased": dict(),
+  "fused": dict(MQ_COLSUM_FUSED=1),
+  "phased_triv": dict(MQ_TRIVIAL_SOLVE=1),
 }
 for name, d in V.items():
     flags = [f"-D{k}={v}" for k, v in d.items()]
