@@ -32,8 +32,8 @@
 extern "C" {
 #endif
 
-#define MQ_ABI_VERSION 1
-#define MQ_TILE_ENTRIES 2048 /* entries staged per shared-memory tile (default build) */
+#define MQ_ABI_VERSION 2
+#define MQ_TILE_ENTRIES 2816 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
 
@@ -95,6 +95,9 @@ typedef struct mq_state {
     int64_t *navg;    /* [1]  inner iterations since the last restart          */
     int64_t *pass_out;/* [iters] per-iteration row-solver work counter         */
     int64_t *faults;  /* [1]  rows whose solver failed                         */
+    double *srow;     /* [n] [pad] per-buyer utility after the last prox: the
+                         row solve's warm start (<= 0: none; any value is
+                         correct, a close one saves sweeps)                    */
 } mq_state;
 
 /* ---- faithful drop-in ------------------------------------------------------

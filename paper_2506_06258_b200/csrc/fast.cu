@@ -38,11 +38,15 @@
 #ifndef MQ_NGW
 #define MQ_NGW 0
 #endif
+// Shared memory is sized so that the unified L1 keeps >= 60 KB: random
+// gathers (p[col], the column sums' x) need L1 lines to track their misses,
+// and their throughput halves when the carveout leaves ~28 KB (tools/micro/
+// gather_l1.cu).  Two large stages beat three small ones.
 #ifndef MQ_ETILE
 #define MQ_ETILE MQ_TILE_ENTRIES
 #endif
 #ifndef MQ_STAGES
-#define MQ_STAGES 3
+#define MQ_STAGES 2
 #endif
 #ifndef MQ_LAG
 #define MQ_LAG 4
@@ -62,6 +66,9 @@
 #ifndef MQ_CS_CHUNK
 #define MQ_CS_CHUNK 512
 #endif
+#ifndef MQ_SMEM_PAD
+#define MQ_SMEM_PAD 0  /* experiment: extra dynamic shared memory (shrinks L1) */
+#endif
 #ifndef MQ_WAIT_HINT_NS
 #define MQ_WAIT_HINT_NS 0
 #endif
@@ -75,11 +82,25 @@ constexpr int kMaxSweeps = 4096;
 // 3 column-sum warps waiting for a block, 4 column-sum gather cycles
 __device__ unsigned long long g_wait_cycles[8];
 #ifdef MQ_PROFILE_WAITS
+// per-thread accumulation, flushed once when the kernel's scope ends
+struct ProfAcc {
+    unsigned long long v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    __device__ ~ProfAcc() {
+        for (int i = 0; i < 8; ++i)
+            if (v[i]) atomicAdd(&g_wait_cycles[i], v[i]);
+    }
+};
+#define MQ_PROF_DECL() ProfAcc _prof
 #define MQ_T0() const long long _t0 = clock64()
-#define MQ_T1(slot) atomicAdd(&g_wait_cycles[slot], (unsigned long long)(clock64() - _t0))
+#define MQ_T1(slot) (_prof.v[slot] += (unsigned long long)(clock64() - _t0))
+#define MQ_TS(v) const long long v = clock64()
+#define MQ_TA(slot, a, b) if (wl == 0) _prof.v[slot] += (unsigned long long)((b) - (a))
 #else
+#define MQ_PROF_DECL()
 #define MQ_T0()
 #define MQ_T1(slot)
+#define MQ_TS(v)
+#define MQ_TA(slot, a, b)
 #endif
 
 struct Avg {
@@ -139,6 +160,18 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// price gather p[col]: read-only, L2-resident (m * 8 bytes); optionally kept
+// out of L1 so the gathers do not evict the warps' other L1 lines
+__device__ __forceinline__ double ld_price(const double *a) {
+#ifdef MQ_P_NOALLOC
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(a));
+    return v;
+#else
+    return __ldg(a);
+#endif
 }
 
 // ------------------------------------------------------------ price step
@@ -291,6 +324,94 @@ __device__ __forceinline__ double row_root_regs(const double (&c)[PER], const do
     return s;
 }
 
+// Warm-started variant for rows held in registers.  s0 = the row's utility
+// after the previous prox (srow; <= 0: none).  The first sweep evaluates the
+// active set at s0: if g(s0) >= s0, s0 is below the root and the root of that
+// set (or s0) is the next lower bound; otherwise g(s0) < s0 is itself a lower
+// bound (g is nonincreasing).  Later sweeps compare each lane's active mask
+// with the previous one (a ballot, no reduction) and reduce A, B only when
+// the set changed, so a row whose set is already right costs one reduction.
+template <int G, int PER>
+__device__ __forceinline__ double row_root_warm(const double (&c)[PER], const double (&u)[PER],
+                                                double tw, double s0, bool active_row,
+                                                uint32_t gmask, int *sweeps, bool *ok) {
+    auto amask = [&](double q) -> uint32_t {
+        uint32_t msk = 0;
+#pragma unroll
+        for (int e = 0; e < PER; ++e)
+            if (u[e] > 0.0 && fma(c[e], q, tw * u[e]) > 0.0) msk |= 1u << e;
+        return msk;
+    };
+    auto sums = [&](uint32_t msk, double &As, double &Bs) {
+        double a_ = 0.0, b_ = 0.0;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            if ((msk >> e) & 1u) {
+                a_ += u[e] * c[e];
+                b_ += u[e] * u[e];
+            }
+        }
+        As = group_sum<G>(a_);
+        Bs = group_sum<G>(b_);
+    };
+    bool done = !active_row;
+    double s = 1.0;
+    uint32_t prev = 0;
+    bool force = false;
+    int nsw = 0;
+    {
+        const bool warm = s0 > 0.0;
+        const uint32_t msk = amask(warm ? s0 : 0.0);  // s0 <= 0: every u > 0 entry
+        double A0, B0;
+        sums(msk, A0, B0);
+        const bool any = (__ballot_sync(MQ_FULL, msk != 0u) & gmask) != 0u;
+        if (!done) {
+            ++nsw;
+            if (!warm) {
+                if (any) {
+                    s = active_root(A0, B0, tw);
+                    prev = msk;
+                } else {
+                    done = true;  // no entry with u > 0
+                }
+            } else {
+                const double g0 = A0 + tw * B0 / s0;
+                if (g0 >= s0) {
+                    s = fmax(active_root(A0, B0, tw), s0);
+                    prev = msk;
+                } else {
+                    s = g0;  // lower bound; its active set is still unknown
+                    force = true;
+                }
+            }
+        }
+    }
+    for (int k = 0; k < kMaxSweeps; ++k) {
+        if (!__any_sync(MQ_FULL, !done)) break;
+        const uint32_t msk = amask(s);
+        const bool chg = (__ballot_sync(MQ_FULL, msk != prev || force) & gmask) != 0u;
+        const bool any = (__ballot_sync(MQ_FULL, msk != 0u) & gmask) != 0u;
+        bool need = false;
+        if (!done) {
+            ++nsw;
+            if (!chg || !any) done = true;  // s is the root of its own active set
+            else need = true;
+        }
+        if (__any_sync(MQ_FULL, need)) {
+            double As, Bs;
+            sums(msk, As, Bs);
+            if (need) {
+                s = fmax(active_root(As, Bs, tw), s);
+                prev = msk;
+                force = false;
+            }
+        }
+    }
+    *sweeps = nsw;
+    *ok = done;
+    return s;
+}
+
 // ------------------------------------------------------------ primal (fused)
 #ifdef MQ_SCATTER
 constexpr bool kScatter = true;       // column sums from a column-major copy of x
@@ -307,7 +428,19 @@ constexpr bool kPhased = true;        // solve a block of tiles, grid barrier, g
 #else
 constexpr bool kPhased = false;       // default: column-sum warps gather concurrently (fused)
 #endif
-constexpr int kPhChunk = 4096;        // gathered values staged per round (phased mode)
+constexpr int kPhChunk = 4096;
+#ifdef MQ_X_DIRECT
+constexpr bool kXDirect = true;   // x is L2-prefetched and loaded by the solvers, not staged
+#else
+constexpr bool kXDirect = false;
+#endif
+#ifdef MQ_XB_DIRECT
+constexpr bool kXBDirect = true;  // xbar likewise
+#else
+constexpr bool kXBDirect = false;
+#endif
+static_assert(!(kXDirect || kXBDirect) || (MQ_NGW == 0 && !kPhased && !kScatter && !kSplit),
+              "direct x/xbar loads: default (fused) mode only");        // gathered values staged per round (phased mode)
 
 template <int ETILE, int RTILE, bool HASC>
 struct TileLayout {
@@ -316,14 +449,15 @@ struct TileLayout {
     // (c = x - tau p[col] is written by the gather warps, not by TMA)
     static constexpr int kU = 0;
     static constexpr int kX = kU + (ETILE + 2) * 8;
-    static constexpr int kXB = kX + (ETILE + 2) * 8;
-    static constexpr int kC = kXB + (ETILE + 2) * 8;
+    static constexpr int kXB = kX + (kXDirect ? 0 : (ETILE + 2) * 8);
+    static constexpr int kC = kXB + (kXBDirect ? 0 : (ETILE + 2) * 8);
     static constexpr int kCol = kC + (HASC ? (ETILE + 2) * 8 : 0);
     static constexpr int kTp = kCol + (ETILE + 4) * 4;       // tpos (scatter mode)
     static constexpr int kRp = kTp + (kScatter ? (ETILE + 4) * 4 : 0);
     static constexpr int kW = kRp + (RTILE + 4) * 8;
-    static constexpr int kStage = (kW + (RTILE + 2) * 8 + 127) / 128 * 128;
-    static_assert(kX % 16 == 0 && kCol % 16 == 0 && kRp % 16 == 0 && kW % 16 == 0,
+    static constexpr int kS = kW + (RTILE + 2) * 8;  // srow: warm-start utilities
+    static constexpr int kStage = (kS + (RTILE + 2) * 8 + 127) / 128 * 128;
+    static_assert(kX % 16 == 0 && kCol % 16 == 0 && kRp % 16 == 0 && kW % 16 == 0 && kS % 16 == 0,
                   "bulk-copy destinations must be 16-byte aligned");
 };
 
@@ -342,6 +476,15 @@ __device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32
         " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
         "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
         : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// coherent load that does not allocate in L1 (streams read once by this thread)
+__device__ __forceinline__ double ld_na(const double *a) {
+    double v;
+    asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(a) : "memory");
+    return v;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
@@ -372,7 +515,10 @@ constexpr bool kCsPerWarp = true;     // each column-sum warp publishes its prog
 #else
 constexpr bool kCsPerWarp = false;    // one publication per CTA
 #endif
-constexpr int kCsCap = 10240;         // staged bperm entries per CTA (CTA-level column sums)
+#ifndef MQ_CS_CAP
+#define MQ_CS_CAP 4096
+#endif
+constexpr int kCsCap = MQ_CS_CAP;         // staged bperm entries per CTA (CTA-level column sums)
 constexpr int kCsChunk = MQ_CS_CHUNK; // bperm entries per staged column-sum chunk (per warp)
 constexpr int kWCols = MQ_NCW >= 4 ? 320 : 600;  // goods per column-sum warp
 constexpr int kClaim = MQ_CLAIM;      // tiles claimed per atomic by a producer
@@ -492,6 +638,7 @@ __global__ void __launch_bounds__((NSW + NGW + NCW + 1) * 32, 1)
 primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
                     int write_cs, int64_t tile_lo, int64_t tile_hi, int *tile_ctr) {
     using L = TileLayout<ETILE, RTILE, (NGW > 0)>;
+    MQ_PROF_DECL();
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTAGE * L::kStage);
     uint64_t *empty = full + NSTAGE;
@@ -570,9 +717,12 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                         aligned_span<8>(st.x, e0, cnt, &src_x, &b8);
                         aligned_span<8>(st.xbar, e0, cnt, &src_xb, &b8);
                         aligned_span<4>(mk.col, e0, cnt, &src_c, &b4);
-                        mbar_expect_tx(&full[s], brp + bw + (cnt > 0 ? 3 * b8 + b4 : 0));
+                        const unsigned char *src_s;
+                        aligned_span<8>(st.srow, r0, r1 - r0, &src_s, &bw);
+                        mbar_expect_tx(&full[s], brp + 2 * bw + (cnt > 0 ? 3 * b8 + b4 : 0));
                         bulk_g2s(base + L::kRp, src_rp, brp, &full[s]);
                         bulk_g2s(base + L::kW, src_w, bw, &full[s]);
+                        bulk_g2s(base + L::kS, src_s, bw, &full[s]);
                         if (cnt > 0) {
                             bulk_g2s_hint(base + L::kU, src_u, b8, &full[s], pol);
                             bulk_g2s(base + L::kX, src_x, b8, &full[s]);
@@ -646,13 +796,19 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 aligned_span<4>(mk.col, e0, cnt, &src_c, &b4);
                 const unsigned char *src_tp = nullptr;
                 if (kScatter) aligned_span<4>(mk.tpos, e0, cnt, &src_tp, &b4);
-                mbar_expect_tx(&full[s], brp + bw + (cnt > 0 ? 3 * b8 + (kScatter ? 2 : 1) * b4 : 0));
+                constexpr int n8 = 1 + (kXDirect ? 0 : 1) + (kXBDirect ? 0 : 1);
+                const unsigned char *src_s;
+                aligned_span<8>(st.srow, r0, r1 - r0, &src_s, &bw);
+                mbar_expect_tx(&full[s], brp + 2 * bw + (cnt > 0 ? n8 * b8 + (kScatter ? 2 : 1) * b4 : 0));
                 bulk_g2s(base + L::kRp, src_rp, brp, &full[s]);
                 bulk_g2s(base + L::kW, src_w, bw, &full[s]);
+                bulk_g2s(base + L::kS, src_s, bw, &full[s]);
                 if (cnt > 0) {
                     bulk_g2s_hint(base + L::kU, src_u, b8, &full[s], pol);
-                    bulk_g2s(base + L::kX, src_x, b8, &full[s]);
-                    bulk_g2s_hint(base + L::kXB, src_xb, b8, &full[s], pol);
+                    if (kXDirect) prefetch_l2(src_x, b8);
+                    else bulk_g2s(base + L::kX, src_x, b8, &full[s]);
+                    if (kXBDirect) prefetch_l2(src_xb, b8);
+                    else bulk_g2s_hint(base + L::kXB, src_xb, b8, &full[s], pol);
                     bulk_g2s_hint(base + L::kCol, src_c, b4, &full[s], pol);
                     if (kScatter) bulk_g2s_hint(base + L::kTp, src_tp, b4, &full[s], pol);
                 }
@@ -687,7 +843,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
 #pragma unroll
                     for (int q = 0; q < U; ++q) {
                         const int t = t0 + q * NGW * 32;
-                        pv[q] = t < cnt ? __ldg(st.p + scol[t]) : 0.0;
+                        pv[q] = t < cnt ? ld_price(st.p + scol[t]) : 0.0;
                     }
 #pragma unroll
                     for (int q = 0; q < U; ++q) {
@@ -1007,10 +1163,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
     // ---------------------------------------------------------- solvers
     const int lane = tid & (G - 1);
     const int gsub = wl / G;
-    const uint64_t pkeep = policy_evict_last();
+    const uint64_t pkeep = kScatter ? policy_evict_last() : 0;
     const Avg av = avg_weights(st.navg, it);
-    int64_t my_sweeps = 0;
-    int64_t my_faults = 0;
+    int my_sweeps = 0;  // per warp and launch: < 2^31
+    int my_faults = 0;
     int64_t ph_blk = 0;
     for (int64_t j = 0;; ++j) {
         const int s = (int)(j % NSTAGE);
@@ -1047,6 +1203,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         const int lr = (int)(((r0 * 8) & 15) >> 3);
         const int64_t *srp = reinterpret_cast<const int64_t *>(base + L::kRp) + lr;
         const double *sw = reinterpret_cast<const double *>(base + L::kW) + lr;
+        const double *ss = reinterpret_cast<const double *>(base + L::kS) + lr;
         const int64_t e0 = srp[0];
         const int d8 = (int)(((e0 * 8) & 15) >> 3), d4 = (int)(((e0 * 4) & 15) >> 2);
         const double *su = reinterpret_cast<const double *>(base + L::kU) + d8;
@@ -1054,7 +1211,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         const double *sxb = reinterpret_cast<const double *>(base + L::kXB) + d8;
         // c = x - tau p[col]: from the gather warps, or computed here (then
         // written over x in place for the shared-memory path)
-        double *sc = reinterpret_cast<double *>(base + (NGW > 0 ? L::kC : L::kX)) + d8;
+        double *sc = kXDirect ? st.x + e0
+                              : reinterpret_cast<double *>(base + (NGW > 0 ? L::kC : L::kX)) + d8;
+        auto ldx = [&](int t) -> double { return kXDirect ? ld_na(st.x + e0 + t) : sx[t]; };
+        auto ldxb = [&](int t) -> double { return kXBDirect ? ld_na(st.xbar + e0 + t) : sxb[t]; };
         const int32_t *scol = reinterpret_cast<const int32_t *>(base + L::kCol) + d4;
         const int32_t *stp = reinterpret_cast<const int32_t *>(base + L::kTp) + d4;
 
@@ -1077,9 +1237,9 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
 #ifdef MQ_TRIVIAL_SOLVE  // bandwidth experiment: stream the tile, skip the solve
             if (MQ_TRIVIAL_SOLVE == 1) {
                 for (int t = a + lane; t < b; t += G) {
-                    const double xn = sx[t] + 1e-300 * su[t];
+                    const double xn = ldx(t) + 1e-300 * su[t];
                     st.x[e0 + t] = xn;
-                    __stcs(st.xbar + e0 + t, av.wold * sxb[t] + av.wnew * xn);
+                    __stcs(st.xbar + e0 + t, av.wold * ldxb(t) + av.wnew * xn);
                     if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
                 }
             }
@@ -1089,58 +1249,69 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
 #endif
                 // ---- row in registers
                 constexpr int RP = kRegPer > 0 ? kRegPer : 1;
+                MQ_TS(tq0);
                 double c[RP], u[RP];
-                double s0p = 0.0, ap = 0.0, bp = 0.0;
 #pragma unroll
                 for (int e = 0; e < RP; ++e) {
                     const int t = a + lane + e * G;
                     if (t < b) {
-                        const double ue = su[t], xe = sx[t];
+                        const double ue = su[t], xe = ldx(t);
                         double ce;
                         if (NGW > 0) {
                             ce = sc[t];
                         } else {
-                            ce = xe - tau * __ldg(st.p + scol[t]);
+                            ce = xe - tau * ld_price(st.p + scol[t]);
                             if (x_prev_out) x_prev_out[e0 + t] = xe;
                         }
                         u[e] = ue;
                         c[e] = ce;
-                        s0p += ue * xe;
-                        ap += ue * ce;
-                        bp += ue * ue;
                     } else {
                         u[e] = 0.0;
                         c[e] = 0.0;
                     }
                 }
-                const double s0 = group_sum<G>(s0p);
-                const double A = group_sum<G>(ap);
-                const double B = group_sum<G>(bp);
-                const double sr =
-                    row_root_regs<G, RP>(c, u, b - a, tw, s0, A, B, has, &nsw, &ok);
+                const double s0 = has ? ss[r] : 0.0;
+                MQ_TS(tq1);
+                const uint32_t gmask = G == 32 ? MQ_FULL : (((1u << G) - 1u) << (gsub * G));
+                const double sr = row_root_warm<G, RP>(c, u, tw, s0, has, gmask, &nsw, &ok);
+                if (has && lane == 0) st.srow[r0 + r] = sr;
                 const double inv_s = 1.0 / sr;
+                MQ_TS(tq2);
+                constexpr int XP = kXBDirect ? RP : 1;  // direct xbar: all loads in flight first
+                double xb[XP];
+                if (kXBDirect) {
+#pragma unroll
+                    for (int e = 0; e < XP; ++e) {
+                        const int t = a + lane + e * G;
+                        xb[e] = t < b ? ldxb(t) : 0.0;
+                    }
+                }
 #pragma unroll
                 for (int e = 0; e < RP; ++e) {
                     const int t = a + lane + e * G;
                     if (t < b) {
                         const double xn = fmax(c[e] + tw * u[e] * inv_s, 0.0);
                         st.x[e0 + t] = xn;
-                        __stcs(st.xbar + e0 + t, av.wold * sxb[t] + av.wnew * xn);
+                        __stcs(st.xbar + e0 + t, av.wold * (kXBDirect ? xb[e % XP] : ldxb(t)) + av.wnew * xn);
                         if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
                     }
                 }
+                MQ_TS(tq3);
+                MQ_TA(5, tq0, tq1);
+                MQ_TA(6, tq1, tq2);
+                MQ_TA(7, tq2, tq3);
             } else if (!kTrivial) {
                 // ---- longer rows: stream the row from shared memory
                 double s0p = 0.0, ap = 0.0, bp = 0.0;
                 for (int t = a + lane; t < b; t += G) {
-                    const double ue = su[t], xe = sx[t];
+                    const double ue = su[t], xe = ldx(t);
                     double ce;
                     if (NGW > 0) {
                         ce = sc[t];
                     } else {
-                        ce = xe - tau * __ldg(st.p + scol[t]);
+                        ce = xe - tau * ld_price(st.p + scol[t]);
                         if (x_prev_out) x_prev_out[e0 + t] = xe;
-                        sc[t] = ce;  // == sx[t]: this lane's entry only
+                        sc[t] = ce;  // over x (shared stage or global): this lane's entry only
                     }
                     s0p += ue * xe;
                     ap += ue * ce;
@@ -1151,16 +1322,17 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 const double B = group_sum<G>(bp);
                 const double sr =
                     row_root_exact<G>(su, sc, a, b, lane, tw, s0, A, B, has, &nsw, &ok);
+                if (has && lane == 0) st.srow[r0 + r] = sr;
                 const double inv_s = 1.0 / sr;
                 for (int t = a + lane; t < b; t += G) {
                     const double xn = fmax(sc[t] + tw * su[t] * inv_s, 0.0);
                     st.x[e0 + t] = xn;
-                    __stcs(st.xbar + e0 + t, av.wold * sxb[t] + av.wnew * xn);
+                    __stcs(st.xbar + e0 + t, av.wold * ldxb(t) + av.wnew * xn);
                     if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
                 }
                 // c was written over x in this stage: order those generic-proxy
                 // writes before the producer's next bulk copy into the stage
-                if (NGW == 0) fence_proxy_async();
+                if (NGW == 0 && !kXDirect) fence_proxy_async();
             }
             if (has && b > a && lane == 0) {
                 my_sweeps += nsw;
@@ -1441,7 +1613,7 @@ constexpr int kQMax = (1152 + kNCW * 32 - 1) / (kNCW * 32);  // goods per column
 #endif
 using PrimalLayout = TileLayout<kEtile, MQ_TILE_ROWS, (kNGW > 0)>;
 
-constexpr int kPrimalSmem = kStages * PrimalLayout::kStage + 7 * kStages * 8 + 4 * kStages * 4 + 128 +
+constexpr int kPrimalSmem = MQ_SMEM_PAD + kStages * PrimalLayout::kStage + 7 * kStages * 8 + 4 * kStages * 4 + 128 +
                             (kPhased ? kPhChunk * 8 : (kScatter || kSplit) ? 0 :
 #ifdef MQ_CS_PERWARP
                              kNCW * (((2 * (kCsChunk + 8) + 2 * (kWCols + 8)) * 4 + kCsChunk * 8 +

@@ -16,6 +16,7 @@ Built once per instance (or per row shard); every later call only passes the
 `mq_market` struct of raw pointers to the native library.
 """
 
+import os
 import ctypes
 import warnings
 
@@ -82,7 +83,7 @@ def build_tiles(row_ptr, tile_entries=nat.TILE_ENTRIES, long_row=nat.LONG_ROW,
     return tiles, long_rows
 
 
-TILES_PER_CTA_PER_BLOCK = 4
+TILES_PER_CTA_PER_BLOCK = int(os.environ.get("MQ_TILES_PER_CTA", "4"))  # tuning override
 
 
 def build_transpose(col, m):

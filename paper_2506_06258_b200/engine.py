@@ -130,6 +130,9 @@ class PdhcgEngine:
         self.x = self._x_buf[:nnz]
         self.xbar = self._xbar_buf[:nnz]
         self.x0 = torch.zeros(nnz, **f64)
+        # per-buyer utility of the last prox: the fused row solve's warm start
+        self._srow_buf = torch.zeros(dm.n + nat.PAD, **f64)
+        self.srow = self._srow_buf[:dm.n]
         # per block: tiles solved, then column-sum warps done (throttle)
         self.blk_done = torch.zeros(2 * dm.nblk + 1, dtype=torch.int32, device=dev)
         # column-major copy of x (only for a scatter-mode build)
@@ -165,7 +168,7 @@ class PdhcgEngine:
             return None
         s = nat.MqState()
         for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "blk_done", "xc",
-                     "steps", "faults"):
+                     "steps", "faults", "srow"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.navg = self.navg_dev.data_ptr()
         s.pass_out = self.pass_buf.data_ptr()
@@ -189,6 +192,7 @@ class PdhcgEngine:
         """Start (or warm start) from allocation x and prices p."""
         self.x.copy_(torch.as_tensor(x, dtype=torch.float64))
         self.p.copy_(torch.as_tensor(p, dtype=torch.float64))
+        self.srow.zero_()  # cold row-solve start: results depend only on (x, p)
         self.xbar.copy_(self.x)
         self.pbar.copy_(self.p)
         if self.mode == "ksection":
@@ -204,6 +208,7 @@ class PdhcgEngine:
         """Mid-run state of kernels.pdhcg_chunk's argument list (lockstep tests)."""
         f = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.float64)  # noqa: E731
         self.x.copy_(f(x))
+        self.srow.zero_()
         self.p.copy_(f(p))
         self.xbar.copy_(f(xbar))
         self.pbar.copy_(f(pbar))
