@@ -73,6 +73,13 @@ typedef struct mq_market {
     const int32_t *tpos;     /* [nnz] [pad]                                     */
     const int64_t *tptr;     /* [m+1]                                           */
     int64_t row_begin;       /* first global row of this shard (0 on 1 GPU)    */
+    /* bucketed column sums (default build): entry e of block b is the
+       bpos[e]-th entry of the block's bperm order; the primal kernel stores
+       x_e there in an L2-resident bucket of bcap doubles (one of
+       mq_bucket_slots() rotating buckets), the column-sum warps then read each
+       good's segment contiguously                                             */
+    const int32_t *bpos;     /* [nnz] [pad]                                     */
+    int64_t bcap;            /* entries of the largest block                    */
 } mq_market;
 
 /* Mutable iterate of the fast (graph-captured) path.  cs / cs_prev / csbar are
@@ -95,6 +102,7 @@ typedef struct mq_state {
     int64_t *navg;    /* [1]  inner iterations since the last restart          */
     int64_t *pass_out;/* [iters] per-iteration row-solver work counter         */
     int64_t *faults;  /* [1]  rows whose solver failed                         */
+    double *bucket;   /* [mq_bucket_slots() * bcap] column-sum buckets (scratch) */
     double *srow;     /* [n] [pad] per-buyer utility after the last prox: the
                          row solve's warm start (<= 0: none; any value is
                          correct, a close one saves sweeps)                    */
@@ -219,6 +227,8 @@ int64_t mq_scratch_doubles(void);
 
 const char *mq_last_error(void);
 int mq_abi_version(void);
+/* rotating column-sum buckets the default build needs (0: none) */
+int mq_bucket_slots(void);
 
 #ifdef __cplusplus
 }

@@ -41,13 +41,14 @@ class MqMarket(ctypes.Structure):
                 ("row_ptr", P), ("col", P), ("u", P), ("u_orig", P), ("w", P),
                 ("tiles", P), ("ntiles", I64), ("long_rows", P), ("nlong", I64),
                 ("bperm", P), ("bptr", P), ("nblk", I64), ("tiles_per_block", I64),
-                ("prim_grid", ctypes.c_int32), ("tpos", P), ("tptr", P), ("row_begin", I64)]
+                ("prim_grid", ctypes.c_int32), ("tpos", P), ("tptr", P), ("row_begin", I64),
+                ("bpos", P), ("bcap", I64)]
 
 
 class MqState(ctypes.Structure):
     _fields_ = [("x", P), ("xbar", P), ("p", P), ("pbar", P), ("cs", P), ("cs_prev", P),
                 ("csbar", P), ("blk_done", P), ("xc", P), ("steps", P), ("navg", P),
-                ("pass_out", P), ("faults", P), ("srow", P)]
+                ("pass_out", P), ("faults", P), ("bucket", P), ("srow", P)]
 
 
 PM = ctypes.POINTER(MqMarket)
@@ -77,6 +78,7 @@ _SIGS = {
     "mq_colsum_mode": (CINT, []),
     "mq_last_error": (ctypes.c_char_p, []),
     "mq_abi_version": (CINT, []),
+    "mq_bucket_slots": (CINT, []),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -80,13 +80,13 @@ constexpr int kMaxSweeps = 4096;
 // cycle counters of the fused kernel's waits (mq_debug_counters): 0 solver
 // waiting for a tile, 1 solver throttled, 2 producer waiting for a free stage,
 // 3 column-sum warps waiting for a block, 4 column-sum gather cycles
-__device__ unsigned long long g_wait_cycles[8];
+__device__ unsigned long long g_wait_cycles[16];
 #ifdef MQ_PROFILE_WAITS
 // per-thread accumulation, flushed once when the kernel's scope ends
 struct ProfAcc {
-    unsigned long long v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long v[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     __device__ ~ProfAcc() {
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 16; ++i)
             if (v[i]) atomicAdd(&g_wait_cycles[i], v[i]);
     }
 };
@@ -117,6 +117,11 @@ __device__ __forceinline__ Avg avg_weights(const int64_t *navg, int it) {
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
 }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
@@ -160,6 +165,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// order generic-proxy global writes (observed through an acquire) before
+// this thread's subsequent bulk copies from global memory
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // price gather p[col]: read-only, L2-resident (m * 8 bytes); optionally kept
@@ -331,15 +341,18 @@ __device__ __forceinline__ double row_root_regs(const double (&c)[PER], const do
 // bound (g is nonincreasing).  Later sweeps compare each lane's active mask
 // with the previous one (a ballot, no reduction) and reduce A, B only when
 // the set changed, so a row whose set is already right costs one reduction.
-template <int G, int PER>
-__device__ __forceinline__ double row_root_warm(const double (&c)[PER], const double (&u)[PER],
+// u(e): the lane's e-th utility (registers, or re-read from shared memory)
+template <int G, int PER, class UF>
+__device__ __forceinline__ double row_root_warm(const double (&c)[PER], UF u,
                                                 double tw, double s0, bool active_row,
                                                 uint32_t gmask, int *sweeps, bool *ok) {
     auto amask = [&](double q) -> uint32_t {
         uint32_t msk = 0;
 #pragma unroll
-        for (int e = 0; e < PER; ++e)
-            if (u[e] > 0.0 && fma(c[e], q, tw * u[e]) > 0.0) msk |= 1u << e;
+        for (int e = 0; e < PER; ++e) {
+            const double ue = u(e);
+            if (ue > 0.0 && fma(c[e], q, tw * ue) > 0.0) msk |= 1u << e;
+        }
         return msk;
     };
     auto sums = [&](uint32_t msk, double &As, double &Bs) {
@@ -347,8 +360,9 @@ __device__ __forceinline__ double row_root_warm(const double (&c)[PER], const do
 #pragma unroll
         for (int e = 0; e < PER; ++e) {
             if ((msk >> e) & 1u) {
-                a_ += u[e] * c[e];
-                b_ += u[e] * u[e];
+                const double ue = u(e);
+                a_ += ue * c[e];
+                b_ += ue * ue;
             }
         }
         As = group_sum<G>(a_);
@@ -418,12 +432,22 @@ constexpr bool kScatter = true;       // column sums from a column-major copy of
 #else
 constexpr bool kScatter = false;
 #endif
+#ifdef MQ_CS_ATOMIC
+constexpr bool kAtomic = true;        // experiment: fixed-point integer atomics per entry
+#else
+constexpr bool kAtomic = false;
+#endif
+#ifdef MQ_CS_BUCKET
+constexpr bool kBucket = !kScatter;   // solvers store x into L2 buckets in column order
+#else
+constexpr bool kBucket = false;
+#endif
 #ifdef MQ_COLSUM_SPLIT
-constexpr bool kSplit = !kScatter;    // per block of tiles: primal launch, then gather launch
+constexpr bool kSplit = !kScatter && !kBucket;  // per block of tiles: primal launch, then gather launch
 #else
 constexpr bool kSplit = false;
 #endif
-#if defined(MQ_COLSUM_PHASED) && !defined(MQ_COLSUM_SPLIT) && !defined(MQ_SCATTER)
+#if defined(MQ_COLSUM_PHASED) && !defined(MQ_COLSUM_SPLIT) && !defined(MQ_SCATTER) && !defined(MQ_CS_BUCKET)
 constexpr bool kPhased = true;        // solve a block of tiles, grid barrier, gather it from L2
 #else
 constexpr bool kPhased = false;       // default: column-sum warps gather concurrently (fused)
@@ -452,8 +476,8 @@ struct TileLayout {
     static constexpr int kXB = kX + (kXDirect ? 0 : (ETILE + 2) * 8);
     static constexpr int kC = kXB + (kXBDirect ? 0 : (ETILE + 2) * 8);
     static constexpr int kCol = kC + (HASC ? (ETILE + 2) * 8 : 0);
-    static constexpr int kTp = kCol + (ETILE + 4) * 4;       // tpos (scatter mode)
-    static constexpr int kRp = kTp + (kScatter ? (ETILE + 4) * 4 : 0);
+    static constexpr int kTp = kCol + (ETILE + 4) * 4;       // tpos (scatter) / bpos (bucket)
+    static constexpr int kRp = kTp + ((kScatter || kBucket) ? (ETILE + 4) * 4 : 0);
     static constexpr int kW = kRp + (RTILE + 4) * 8;
     static constexpr int kS = kW + (RTILE + 2) * 8;  // srow: warm-start utilities
     static constexpr int kStage = (kS + (RTILE + 2) * 8 + 127) / 128 * 128;
@@ -529,6 +553,10 @@ constexpr bool kTrivial = true;       // bandwidth experiments only
 constexpr bool kTrivial = false;
 #endif
 constexpr int kCsCols = 1152;         // goods per CTA (>= QMAX * NCW * 32)
+#ifndef MQ_BK_CHUNK
+#define MQ_BK_CHUNK 1024
+#endif
+constexpr int kBkChunk = MQ_BK_CHUNK; // bucket entries per staged chunk (bucket mode)
 constexpr int kCsQ = MQ_CSQ, kCsU = MQ_CSU;  // goods x gathers in flight per column-sum thread
 constexpr int64_t kLag = MQ_LAG;      // solver blocks ahead of the slowest column-sum CTA
 constexpr int64_t kSpinLimit = 4000000000ll;  // ~2 s of clock64: a stalled block is a fault
@@ -795,11 +823,13 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 aligned_span<8>(st.xbar, e0, cnt, &src_xb, &b8);
                 aligned_span<4>(mk.col, e0, cnt, &src_c, &b4);
                 const unsigned char *src_tp = nullptr;
-                if (kScatter) aligned_span<4>(mk.tpos, e0, cnt, &src_tp, &b4);
+                if (kScatter || kBucket)
+                    aligned_span<4>(kScatter ? mk.tpos : mk.bpos, e0, cnt, &src_tp, &b4);
                 constexpr int n8 = 1 + (kXDirect ? 0 : 1) + (kXBDirect ? 0 : 1);
                 const unsigned char *src_s;
                 aligned_span<8>(st.srow, r0, r1 - r0, &src_s, &bw);
-                mbar_expect_tx(&full[s], brp + 2 * bw + (cnt > 0 ? n8 * b8 + (kScatter ? 2 : 1) * b4 : 0));
+                mbar_expect_tx(&full[s], brp + 2 * bw +
+                                             (cnt > 0 ? n8 * b8 + ((kScatter || kBucket) ? 2 : 1) * b4 : 0));
                 bulk_g2s(base + L::kRp, src_rp, brp, &full[s]);
                 bulk_g2s(base + L::kW, src_w, bw, &full[s]);
                 bulk_g2s(base + L::kS, src_s, bw, &full[s]);
@@ -810,7 +840,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     if (kXBDirect) prefetch_l2(src_xb, b8);
                     else bulk_g2s_hint(base + L::kXB, src_xb, b8, &full[s], pol);
                     bulk_g2s_hint(base + L::kCol, src_c, b4, &full[s], pol);
-                    if (kScatter) bulk_g2s_hint(base + L::kTp, src_tp, b4, &full[s], pol);
+                    if (kScatter || kBucket) bulk_g2s_hint(base + L::kTp, src_tp, b4, &full[s], pol);
                 }
             }
 
@@ -885,6 +915,123 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             for (int q = 0; q < PQ; ++q) {
                 const int jl = pt + q * NP;
                 if (jl < ph_nc) st.cs[ph_lo + jl] = ph_acc[q];
+            }
+        }
+        return;
+    }
+    if (kAtomic && warp > NSW + NGW) return;
+    if (kBucket && warp > NSW + NGW) {  // ---------------- column sums (buckets)
+        // The CTA's NCW column-sum warps own goods [j_lo, j_hi).  The solvers
+        // stored every x of block b at its bpos slot of bucket b % kLag, so the
+        // owned goods' values of the block are one contiguous bucket range,
+        // in good order and ascending rows inside a good.  Once every CTA has
+        // solved the block, the range streams through shared memory in
+        // chunks (TMA bulk copies from L2, double-buffered), and each thread
+        // adds its goods' values in order (deterministic, the reference's
+        // column_sums order).
+        const int ct = tid - (NSW + NGW + 1) * 32;
+        const int64_t per = (mk.m + gridDim.x - 1) / gridDim.x;
+        const int64_t j_lo = blockIdx.x * per;
+        const int64_t j_hi = j_lo + per < mk.m ? j_lo + per : mk.m;
+        const int nc = (int)(j_hi > j_lo ? j_hi - j_lo : 0);
+        int32_t *sbptr = cstage;                                             // [kCsCols + 8]
+        double *sval = reinterpret_cast<double *>(cstage + kCsCols + 8);     // [2][kBkChunk + 4]
+        uint64_t *cbar = reinterpret_cast<uint64_t *>(sval + 2 * (kBkChunk + 4));  // chunks 0/1, bptr
+        if (ct == 0) {
+            mbar_init(&cbar[0], 1);
+            mbar_init(&cbar[1], 1);
+            mbar_init(&cbar[2], 1);
+            mbar_fence_init();
+        }
+        colsum_sync(NCW);
+        if (nc == 0) {  // no goods here: still publish progress for the throttle
+            if (ct == 0)
+                for (int64_t b = 0; b < mk.nblk; ++b) atomicAdd(st.blk_done + mk.nblk + b, 1);
+            return;
+        }
+        auto stage_ptr = [&](int64_t b) {  // bptr slice of the owned goods (one thread)
+            const unsigned char *src;
+            uint32_t bytes;
+            aligned_span<4>(mk.bptr, b * mk.m + j_lo, nc + 1, &src, &bytes);
+            mbar_expect_tx(&cbar[2], bytes);
+            bulk_g2s(sbptr, src, bytes, &cbar[2]);
+        };
+        double acc[QMAX];
+#pragma unroll
+        for (int q = 0; q < QMAX; ++q) acc[q] = 0.0;
+        uint32_t use0 = 0, use1 = 0, pphase = 0;
+        if (ct == 0) stage_ptr(0);
+        for (int64_t b = 0; b < mk.nblk; ++b) {
+            const int64_t kb0 = b * tpb_all;
+            const int target = (int)((kb0 + tpb_all < mk.ntiles ? kb0 + tpb_all : mk.ntiles) - kb0);
+            {
+                MQ_T0();
+                if (ct == 0) wait_counter(st.blk_done + b, target, st.faults, true);
+                colsum_sync(NCW);
+                if (ct == 0) MQ_T1(3);
+            }
+            MQ_T0();
+            mbar_wait(&cbar[2], pphase);
+            pphase ^= 1u;
+            const int32_t *bp = sbptr + (int)((((b * mk.m + j_lo) * 4) & 15) >> 2);
+            const int64_t base = __ldg(mk.bptr + b * mk.m);  // the block's first position
+            const int64_t rlo = bp[0] - base, rhi = bp[nc] - base;
+            const double *slot = st.bucket + (b % kLag) * mk.bcap;
+            const int64_t nch = (rhi - rlo + kBkChunk - 1) / kBkChunk;
+            auto issue = [&](int64_t g) {  // one thread
+                const int buf = (int)(g & 1);
+                const int64_t c0 = rlo + g * kBkChunk;
+                const int64_t c1 = c0 + kBkChunk < rhi ? c0 + kBkChunk : rhi;
+                const unsigned char *src;
+                uint32_t bytes;
+                aligned_span<8>(slot, c0, c1 - c0, &src, &bytes);
+                mbar_expect_tx(&cbar[buf], bytes);
+                bulk_g2s(sval + buf * (kBkChunk + 4), src, bytes, &cbar[buf]);
+            };
+            if (ct == 0) {
+                fence_proxy_async_global();
+                if (nch > 0) issue(0);
+                if (nch > 1) issue(1);
+            }
+            for (int64_t g = 0; g < nch; ++g) {
+                const int buf = (int)(g & 1);
+                mbar_wait(&cbar[buf], (buf ? use1 : use0) & 1u);
+                if (buf) ++use1; else ++use0;
+                const int64_t c0 = rlo + g * kBkChunk;
+                const int64_t c1 = c0 + kBkChunk < rhi ? c0 + kBkChunk : rhi;
+                const double *sv = sval + buf * (kBkChunk + 4) + (int)(c0 & 1) - c0;
+#pragma unroll
+                for (int q = 0; q < QMAX; ++q) {
+                    const int jl = ct + q * NCW * 32;
+                    if (jl >= nc) break;
+                    int64_t t = bp[jl] - base, e = bp[jl + 1] - base;
+                    t = t > c0 ? t : c0;
+                    e = e < c1 ? e : c1;
+                    double a = acc[q];
+                    for (; t < e; ++t) a += sv[t];
+                    acc[q] = a;
+                }
+                colsum_sync(NCW);  // the chunk buffer is consumed
+                if (ct == 0 && g + 2 < nch) {
+                    fence_proxy_async();
+                    issue(g + 2);
+                }
+            }
+            colsum_sync(NCW);  // bp[] reads done
+            if (ct == 0) {
+                MQ_T1(4);
+                atomicAdd(st.blk_done + mk.nblk + b, 1);  // block b summed: its bucket is free
+                if (b + 1 < mk.nblk) {
+                    fence_proxy_async();
+                    stage_ptr(b + 1);
+                }
+            }
+        }
+        if (write_cs) {
+#pragma unroll
+            for (int q = 0; q < QMAX; ++q) {
+                const int jl = ct + q * NCW * 32;
+                if (jl < nc) st.cs[j_lo + jl] = acc[q];
             }
         }
         return;
@@ -1163,7 +1310,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
     // ---------------------------------------------------------- solvers
     const int lane = tid & (G - 1);
     const int gsub = wl / G;
-    const uint64_t pkeep = kScatter ? policy_evict_last() : 0;
+    const uint64_t pkeep = (kScatter || kBucket) ? policy_evict_last() : 0;
     const Avg av = avg_weights(st.navg, it);
     int my_sweeps = 0;  // per warp and launch: < 2^31
     int my_faults = 0;
@@ -1190,7 +1337,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         {
             MQ_T0();
 #if !defined(MQ_NO_COLSUM) && !defined(MQ_CS_NOWAIT)
-            if (!kScatter && !kSplit && !kPhased && blk >= kLag && wl == 0)
+            if (!kScatter && !kSplit && !kPhased && !kAtomic && blk >= kLag && wl == 0)
                 wait_counter(st.blk_done + mk.nblk + (blk - kLag),
                              (int)gridDim.x * (kCsPerWarp ? NCW : 1), st.faults, false);
 #endif
@@ -1217,12 +1364,18 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         auto ldxb = [&](int t) -> double { return kXBDirect ? ld_na(st.xbar + e0 + t) : sxb[t]; };
         const int32_t *scol = reinterpret_cast<const int32_t *>(base + L::kCol) + d4;
         const int32_t *stp = reinterpret_cast<const int32_t *>(base + L::kTp) + d4;
+        double *bslot = kBucket ? st.bucket + (blk % kLag) * mk.bcap : nullptr;
 
+        MQ_TA(13, 0, 1);  // tile visits
         for (;;) {
+            MQ_TS(tc0);
             int rb = 0;
             if (wl == 0) rb = atomicAdd(&claim[s], GPW);
             rb = __shfl_sync(MQ_FULL, rb, 0);
+            MQ_TS(tc1);
+            MQ_TA(8, tc0, tc1);
             if (rb >= nrows) break;  // warp-uniform
+            MQ_TA(12, 0, 1);  // row pairs
             const int r = rb + gsub;
             const bool has = r < nrows;
             int a = 0, b = 0;
@@ -1241,6 +1394,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     st.x[e0 + t] = xn;
                     __stcs(st.xbar + e0 + t, av.wold * ldxb(t) + av.wnew * xn);
                     if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
+                    if (kBucket) st_keep(bslot + stp[t], xn, pkeep);
+                    if (kAtomic)
+                        atomicAdd(reinterpret_cast<unsigned long long *>(st.bucket) + scol[t],
+                                  (unsigned long long)__double2ll_rn(xn * 0x1p40));
                 }
             }
             if (false) {
@@ -1250,6 +1407,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 // ---- row in registers
                 constexpr int RP = kRegPer > 0 ? kRegPer : 1;
                 MQ_TS(tq0);
+                MQ_TA(9, tc1, tq0);
                 double c[RP], u[RP];
 #pragma unroll
                 for (int e = 0; e < RP; ++e) {
@@ -1273,7 +1431,15 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 const double s0 = has ? ss[r] : 0.0;
                 MQ_TS(tq1);
                 const uint32_t gmask = G == 32 ? MQ_FULL : (((1u << G) - 1u) << (gsub * G));
-                const double sr = row_root_warm<G, RP>(c, u, tw, s0, has, gmask, &nsw, &ok);
+#ifdef MQ_U_SMEM
+                // utilities re-read from the stage (fewer live registers per pair)
+                const uint32_t su_l = smem_addr(su + a + lane);
+                const int n_l = b - a - lane > 0 ? (b - a - lane + G - 1) / G : 0;
+                auto uf = [&](int e) -> double { return e < n_l ? lds_f64(su_l + e * G * 8) : 0.0; };
+#else
+                auto uf = [&](int e) -> double { return u[e]; };
+#endif
+                const double sr = row_root_warm<G, RP>(c, uf, tw, s0, has, gmask, &nsw, &ok);
                 if (has && lane == 0) st.srow[r0 + r] = sr;
                 const double inv_s = 1.0 / sr;
                 MQ_TS(tq2);
@@ -1290,10 +1456,18 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 for (int e = 0; e < RP; ++e) {
                     const int t = a + lane + e * G;
                     if (t < b) {
+#ifdef MQ_U_SMEM
+                        const double xn = fmax(c[e] + tw * su[t] * inv_s, 0.0);
+#else
                         const double xn = fmax(c[e] + tw * u[e] * inv_s, 0.0);
+#endif
                         st.x[e0 + t] = xn;
                         __stcs(st.xbar + e0 + t, av.wold * (kXBDirect ? xb[e % XP] : ldxb(t)) + av.wnew * xn);
                         if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
+                    if (kBucket) st_keep(bslot + stp[t], xn, pkeep);
+                    if (kAtomic)
+                        atomicAdd(reinterpret_cast<unsigned long long *>(st.bucket) + scol[t],
+                                  (unsigned long long)__double2ll_rn(xn * 0x1p40));
                     }
                 }
                 MQ_TS(tq3);
@@ -1329,6 +1503,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     st.x[e0 + t] = xn;
                     __stcs(st.xbar + e0 + t, av.wold * ldxb(t) + av.wnew * xn);
                     if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
+                    if (kBucket) st_keep(bslot + stp[t], xn, pkeep);
+                    if (kAtomic)
+                        atomicAdd(reinterpret_cast<unsigned long long *>(st.bucket) + scol[t],
+                                  (unsigned long long)__double2ll_rn(xn * 0x1p40));
                 }
                 // c was written over x in this stage: order those generic-proxy
                 // writes before the producer's next bulk copy into the stage
@@ -1339,6 +1517,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 if (!ok) ++my_faults;
             }
         }
+        MQ_TS(te0);
         __syncwarp();
         if (wl == 0) {
             // the last solver warp out of the tile publishes it (one gpu-scope
@@ -1353,6 +1532,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             }
 #endif
             mbar_arrive(&empty[s]);
+        }
+        {
+            MQ_TS(te1);
+            MQ_TA(10, te0, te1);
         }
     }
     if (kPhased && write_cs) {
@@ -1619,7 +1802,8 @@ constexpr int kPrimalSmem = MQ_SMEM_PAD + kStages * PrimalLayout::kStage + 7 * k
                              kNCW * (((2 * (kCsChunk + 8) + 2 * (kWCols + 8)) * 4 + kCsChunk * 8 +
                                       8 * 8 + 2 * 8 + 127) / 128 * 128)
 #else
-                             (kCsCap + kCsCols + 8) * 4 + 4 * 8 + 16
+                             kBucket ? (kCsCols + 8) * 4 + 2 * (kBkChunk + 4) * 8 + 3 * 8 + 16
+                                     : (kCsCap + kCsCols + 8) * 4 + 4 * 8 + 16
 #endif
                             );
 
@@ -1669,8 +1853,19 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
 }
 
 // adds the long rows (pseudo-block nblk) to cs; csbar update when finalize
+__global__ void cs_from_fixed_kernel(int64_t m, unsigned long long *fix, double *cs) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        cs[j] = (double)(long long)fix[j] * 0x1p-40;
+        fix[j] = 0ull;
+    }
+}
+
 int colsum_rest_launch(const mq_market *mk, const mq_state *st, int it, int finalize,
                        cudaStream_t s) {
+    if (kAtomic)
+        cs_from_fixed_kernel<<<grid_for(mk->m, 256, sm_count() * 8), 256, 0, s>>>(
+            mk->m, reinterpret_cast<unsigned long long *>(st->bucket), st->cs);
     if (kScatter) {
         colsum_xc_kernel<<<grid_for(mk->m, 8, sm_count() * 8), 256, 0, s>>>(
             mk->m, mk->tptr, st->xc, st->cs, finalize ? st->csbar : nullptr, st->navg, it);
@@ -1742,14 +1937,17 @@ int mq_fast_chunk(const mq_market *mk, const mq_state *st, int iters, void *stre
 int mq_debug_counters(unsigned long long *out_host) {
     cudaError_t e = cudaMemcpyFromSymbol(out_host, g_wait_cycles, sizeof(g_wait_cycles));
     if (e != cudaSuccess) return set_error(e, "mq_debug_counters");
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long z[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     e = cudaMemcpyToSymbol(g_wait_cycles, z, sizeof(z));
     return e == cudaSuccess ? 0 : set_error(e, "mq_debug_counters");
 }
 
 int mq_tile_entries(void) { return kEtile; }
 
-int mq_colsum_mode(void) { return kScatter ? 1 : (kSplit ? 2 : (kPhased ? 3 : 0)); }
+int mq_colsum_mode(void) { return kScatter ? 1 : (kSplit ? 2 : (kPhased ? 3 : (kBucket ? 4 : 0))); }
+
+int mq_bucket_slots(void) { return kBucket ? (int)kLag : 0; }
+int mq_fixed_colsum(void) { return kAtomic ? 1 : 0; }
 
 int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream) {
     const int grid = (int)((mk->m + 255) / 256);

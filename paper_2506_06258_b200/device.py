@@ -111,10 +111,14 @@ SPLIT_TILES_PER_BLOCK = 2048   # colsum modes 2/3: ~4M entries (32 MB of x) per 
 
 
 def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
-                           tiles_per_cta=TILES_PER_CTA_PER_BLOCK, tiles_per_block=None):
+                           tiles_per_cta=TILES_PER_CTA_PER_BLOCK, tiles_per_block=None,
+                           with_bpos=False):
     """Entry positions grouped by (block of tiles, good), ascending inside a
     good; long-row entries form the last pseudo-block.  Returns
-    (bperm int32 [nnz], bptr int32 [(nblk+1)*m+1], nblk, tiles_per_block)."""
+    (bperm int32 [nnz], bptr int32 [(nblk+1)*m+1], nblk, tiles_per_block,
+    bpos, bcap): with with_bpos, bpos int32 [nnz + pad] is the inverse of
+    bperm relative to the entry's block start (its slot in the block's
+    column-sum bucket) and bcap the largest tile block; else (None, 0)."""
     dev = col.device
     nnz = col.numel()
     ntiles = int(tiles.shape[0])
@@ -141,7 +145,8 @@ def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
         key = blk.to(torch.int32) * m + col
     else:
         key = blk * m + col.to(torch.int64)
-    del blk
+    if not with_bpos:
+        del blk
     _, perm = torch.sort(key, stable=True)
     # [pad]: the fused kernel stages slices of both arrays with TMA bulk copies
     bperm = torch.zeros(nnz + nat.PAD, dtype=torch.int32, device=dev)
@@ -153,7 +158,20 @@ def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
     torch.cumsum(counts, 0, out=bptr[1:])
     bptr32 = torch.zeros(total + 1 + nat.PAD, dtype=torch.int32, device=dev)
     bptr32[:total + 1] = bptr
-    return bperm[:nnz], bptr32[:total + 1], nblk, tpb
+    bpos, bcap = None, 0
+    if with_bpos:
+        bpos = torch.zeros(nnz + nat.PAD, dtype=torch.int32, device=dev)
+        if nnz:
+            bpos[:nnz].scatter_(0, bperm[:nnz].to(torch.int64),
+                                torch.arange(nnz, dtype=torch.int32, device=dev))
+            base = bptr[torch.arange(nblk + 1, device=dev) * m]  # block starts
+            bpos[:nnz] -= base[blk].to(torch.int32)
+        del blk
+        if nblk:
+            ext = bptr[torch.arange(1, nblk + 1, device=dev) * m] - bptr[
+                torch.arange(nblk, device=dev) * m]
+            bcap = -(-int(ext.max().item()) // 16) * 16  # buckets stay 128-byte aligned
+    return bperm[:nnz], bptr32[:total + 1], nblk, tpb, bpos, bcap
 
 
 class DeviceMarket:
@@ -209,9 +227,11 @@ class DeviceMarket:
             self.tiles = torch.cat([tiles2, self.row_ptr[tiles2]], 1).contiguous()
             self.prim_grid = int(min(max(1, self.tiles.shape[0]), sm_count(dev)))
             mode = int(self.lib.mq_colsum_mode())
-            self.bperm, self.bptr, self.nblk, self.tiles_per_block = build_blocked_schedule(
+            (self.bperm, self.bptr, self.nblk, self.tiles_per_block, self._bpos,
+             self.bcap) = build_blocked_schedule(
                 self.row_ptr, self.col, self.m, tiles2, self.long_rows, self.prim_grid,
-                tiles_per_block=SPLIT_TILES_PER_BLOCK if mode in (2, 3) else None)
+                tiles_per_block=SPLIT_TILES_PER_BLOCK if mode in (2, 3) else None,
+                with_bpos=mode == 4)
             lens = self.row_ptr[1:] - self.row_ptr[:-1]
             self.max_row_len = int(lens.max().item()) if self.n else 0
         self.tperm = self.tptr = None
@@ -254,6 +274,9 @@ class DeviceMarket:
             s.tpos = self._tpos.data_ptr()
             s.tptr = self._tptr_c.data_ptr()
         s.row_begin = self.row_begin
+        if self._bpos is not None:
+            s.bpos = self._bpos.data_ptr()
+        s.bcap = int(self.bcap)
         return s
 
     @classmethod

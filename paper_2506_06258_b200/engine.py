@@ -137,6 +137,13 @@ class PdhcgEngine:
         self.blk_done = torch.zeros(2 * dm.nblk + 1, dtype=torch.int32, device=dev)
         # column-major copy of x (only for a scatter-mode build)
         self.xc = torch.zeros(nnz if getattr(dm, "colsum_mode", 0) == 1 else 1, **f64)
+        # column-sum buckets (bucket-mode build): L2-resident scratch
+        slots = int(dm.lib.mq_bucket_slots()) if hasattr(dm, "lib") else 0
+        nb = slots * int(getattr(dm, "bcap", 0))
+        fixed = getattr(getattr(dm, "lib", None), "mq_fixed_colsum", None)
+        if fixed is not None and fixed() == 1:  # experiment build: fixed-point column sums
+            nb = max(nb, m)
+        self.bucket = torch.zeros(max(1, nb), **f64)
         self.p = torch.zeros(m, **f64)
         self.pbar = torch.zeros(m, **f64)
         self.p0 = torch.zeros(m, **f64)
@@ -168,7 +175,7 @@ class PdhcgEngine:
             return None
         s = nat.MqState()
         for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "blk_done", "xc",
-                     "steps", "faults", "srow"):
+                     "steps", "faults", "srow", "bucket"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.navg = self.navg_dev.data_ptr()
         s.pass_out = self.pass_buf.data_ptr()

@@ -174,6 +174,7 @@ def test_abi_marshaling_without_device():
         "mq_gen_degrees": (0, 1, 10, 0, 0.5, 2.0, 1.0, 1, None, None),
         "mq_tile_entries": (),
         "mq_colsum_mode": (),
+        "mq_bucket_slots": (),
         "mq_gen_fill": (0, 1, 10, 0, 0.5, 2.0, 1.0, 1, None, None, None, None, None),
         "mq_pdhcg_chunk": (0, 0, None, None, None, None, None, None, None, None, None, None,
                            None, 0, 0.1, 0.1, 32, 1e-10, 1, None, None, ctypes.byref(n64), None),
@@ -181,7 +182,10 @@ def test_abi_marshaling_without_device():
     for name, args in calls.items():
         rc = getattr(lib, name)(*args)
         if name == "mq_colsum_mode":
-            assert rc in (0, 1, 2, 3)
+            assert rc in (0, 1, 2, 3, 4)
+            continue
+        if name == "mq_bucket_slots":
+            assert rc >= 0
             continue
         assert rc != 0, name
         if name in ("mq_tile_entries", "mq_colsum_mode"):
@@ -238,10 +242,16 @@ def test_blocked_schedule_preserves_column_order():
     rp, col = _random_csr(rng, n, m, lens)
     rpt = torch.from_numpy(rp)
     tiles, long_rows = build_tiles(rpt, 64, 30, 16)
-    bperm, bptr, nblk, tpb = build_blocked_schedule(rpt, torch.from_numpy(col.astype(np.int32)),
-                                                    m, tiles, long_rows, prim_grid=3,
-                                                    tiles_per_cta=2)
-    bperm, bptr = bperm.numpy(), bptr.numpy()
+    bperm, bptr, nblk, tpb, bpos, bcap = build_blocked_schedule(
+        rpt, torch.from_numpy(col.astype(np.int32)), m, tiles, long_rows, prim_grid=3,
+        tiles_per_cta=2, with_bpos=True)
+    bperm, bptr, bpos = bperm.numpy(), bptr.numpy(), bpos.numpy()[:len(col)]
+    # bpos: each entry's slot in its block's bucket (inverse of bperm, block-relative)
+    starts = bptr[np.arange(nblk + 1) * m]
+    assert bcap == -(-int(np.max(np.diff(starts))) // 16) * 16  # largest tile block, rounded
+    for b in range(nblk + 1):
+        seg = bperm[starts[b]:(starts[b + 1] if b < nblk else len(col))]
+        assert np.array_equal(bpos[seg], np.arange(len(seg)))
     assert tpb == 6 and nblk == -(-tiles.shape[0] // 6)
     assert np.array_equal(np.sort(bperm), np.arange(len(col)))
     row_of = np.repeat(np.arange(n), np.diff(rp))

@@ -16,7 +16,7 @@ shard = bench.shard_rows(cfg, 0, 1, 0)
 dm, eng = bench.make_session(shard, None)
 lib = nat.load_library()
 lib.mq_debug_counters.argtypes = [ctypes.c_void_p]
-buf = (ctypes.c_ulonglong * 8)()
+buf = (ctypes.c_ulonglong * 16)()
 bench.run_iters(eng, 3)
 torch.cuda.synchronize()
 lib.mq_debug_counters(buf)
@@ -30,9 +30,11 @@ ms = e0.elapsed_time(e1) / 10
 cyc = ms * 1e-3 * 1.965e9
 nsm = dm.prim_grid
 names = ["solver wait tile", "solver throttled", "producer wait stage", "colsum wait block",
-         "colsum gather", "solver pass1", "solver root", "solver write"]
+         "colsum gather", "solver pass1", "solver root", "solver write", "solver claim",
+         "solver row meta", "solver tile end"]
 print(f"{cfg}: {ms:.3f} ms/iter, kernel-cycles/SM ~{cyc:.3e}")
-per_warp = {0: 15, 1: 15, 2: 1, 3: 4, 4: 4, 5: 15, 6: 15, 7: 15}
+per_warp = {0: 15, 1: 15, 2: 1, 3: 4, 4: 4, 5: 15, 6: 15, 7: 15, 8: 15, 9: 15, 10: 15}
 for i, nm in enumerate(names):
     v = buf[i] / 10 / nsm / per_warp[i]
     print(f"  {nm:22s} {v:.3e} cycles per warp per iter ({100 * v / cyc:.1f}% of iter)")
+print(f"  row pairs per warp per iter {buf[12] / 10 / nsm / 15:.0f}, tile visits {buf[13] / 10 / nsm / 15:.0f}")
