@@ -190,11 +190,15 @@ class DeviceMarket:
         self.device = dev
 
         def up(a, dtype):
-            if isinstance(a, torch.Tensor):
-                return a.to(device=dev, dtype=dtype).contiguous()
-            with warnings.catch_warnings():
-                warnings.simplefilter("ignore")
-                return torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dtype)
+            # transfer first, convert on the device (a host-side int64 -> int32
+            # pass over 1e9 indices costs seconds)
+            if not isinstance(a, torch.Tensor):
+                from .engine import to_device
+
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore")
+                    a = to_device(a, dev)
+            return a.to(device=dev).to(dtype=dtype).contiguous()
 
         with torch.cuda.device(dev):
             self._rp_buf, self.row_ptr = _padded(up(row_ptr, torch.int64), torch.int64, dev)
@@ -282,7 +286,7 @@ class DeviceMarket:
     @classmethod
     def from_instance(cls, inst, device=None, lib=None):
         u = inst.utilities
-        return cls(u.row_offsets, u.col_indices.astype(np.int32), u.values, inst.budgets,
+        return cls(u.row_offsets, u.col_indices, u.values, inst.budgets,
                    u.n_cols, device=device, lib=lib)
 
     def set_budgets(self, w):

@@ -34,6 +34,78 @@ def _cur_stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+_STAGE_ELEMS = 1 << 24  # 128 MB of float64 per pinned staging buffer
+
+
+def to_host(t):
+    """Device tensor -> numpy, through two pinned staging buffers: the D2H
+    copy of one chunk overlaps the host copy of the previous one (a plain
+    .cpu() of 8 GB goes through pageable memory at a few GB/s)."""
+    n = t.numel()
+    if n * t.element_size() <= (64 << 20):
+        return t.cpu().numpy()
+    t = t.reshape(-1)
+    out = np.empty(n, dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+    stage = [torch.empty(_STAGE_ELEMS, dtype=t.dtype, pin_memory=True) for _ in range(2)]
+    evs = [torch.cuda.Event(), torch.cuda.Event()]
+    prev = None
+    for i, off in enumerate(range(0, n, _STAGE_ELEMS)):
+        c = min(_STAGE_ELEMS, n - off)
+        buf = stage[i & 1]
+        buf[:c].copy_(t[off:off + c], non_blocking=True)
+        evs[i & 1].record()
+        if prev is not None:
+            poff, pc, pi = prev
+            evs[pi & 1].synchronize()
+            _pcopy(out[poff:poff + pc], stage[pi & 1][:pc].numpy())
+        prev = (off, c, i)
+    poff, pc, pi = prev
+    evs[pi & 1].synchronize()
+    _pcopy(out[poff:poff + pc], stage[pi & 1][:pc].numpy())
+    return out
+
+
+def to_device(a, device):
+    """numpy -> device tensor (same dtype) through two pinned staging buffers,
+    the host copy of one chunk overlapping the H2D copy of the previous."""
+    a = np.ascontiguousarray(a).reshape(-1)
+    if a.nbytes <= (64 << 20):
+        return torch.from_numpy(a if a.flags.writeable else a.copy()).to(device)
+    out = torch.empty(a.shape[0], dtype=torch.from_numpy(a[:0].copy()).dtype, device=device)
+    stage = [torch.empty(_STAGE_ELEMS * 8 // a.itemsize, dtype=out.dtype, pin_memory=True)
+             for _ in range(2)]
+    ce = stage[0].numel()
+    evs = [None, None]
+    with torch.cuda.device(out.device):
+        for i, off in enumerate(range(0, a.shape[0], ce)):
+            c = min(ce, a.shape[0] - off)
+            b = i & 1
+            if evs[b] is not None:
+                evs[b].synchronize()  # its previous H2D copy has finished
+            _pcopy(stage[b].numpy()[:c], a[off:off + c])
+            out[off:off + c].copy_(stage[b][:c], non_blocking=True)
+            evs[b] = torch.cuda.Event()
+            evs[b].record()
+        torch.cuda.current_stream().synchronize()
+    return out
+
+
+_POOL = None
+
+
+def _pcopy(dst, src, piece=1 << 21):
+    """np.copyto over threads (numpy drops the GIL; first-touch page faults
+    of a fresh output array dominate a single-threaded copy)."""
+    global _POOL
+    if _POOL is None:
+        import concurrent.futures
+        import os
+
+        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1))
+    n = dst.shape[0]
+    list(_POOL.map(lambda o: np.copyto(dst[o:o + piece], src[o:o + piece]), range(0, n, piece)))
+
+
 class NativeOps:
     """The engine's device operations, each one call into libmarket_eq_b200.so
     on the current CUDA stream (include/market_eq_b200.h)."""
@@ -416,5 +488,5 @@ class PdhcgEngine:
         with np.errstate(divide="ignore"):
             y = w / t
         obj = -float(v[5]) if v[6] == 0 else math.inf
-        return {"prices": self.p.cpu().numpy(), "allocation": self.x.cpu().numpy(),
+        return {"prices": self.p.cpu().numpy(), "allocation": to_host(self.x),
                 "utility_values": t, "dual_values": y, "objective": obj}
