@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define MQ_ABI_VERSION 2
+#define MQ_ABI_VERSION 3
 #define MQ_TILE_ENTRIES 2816 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
@@ -80,6 +80,11 @@ typedef struct mq_market {
        good's segment contiguously                                             */
     const int32_t *bpos;     /* [nnz] [pad]                                     */
     int64_t bcap;            /* entries of the largest block                    */
+    /* fixed-point column sums (default build, mq_colsum_mode() == 5): x_e is
+       added to its good's u64 accumulator as round(x_e * cs_scale) when
+       0 < x_e < cs_xmax (larger values count as faults); cs_scale = 2^k with
+       cs_xmax * cs_scale * (max entries of a good) <= 2^62                    */
+    double cs_scale, cs_xmax;
 } mq_market;
 
 /* Mutable iterate of the fast (graph-captured) path.  cs / cs_prev / csbar are
@@ -102,7 +107,9 @@ typedef struct mq_state {
     int64_t *navg;    /* [1]  inner iterations since the last restart          */
     int64_t *pass_out;/* [iters] per-iteration row-solver work counter         */
     int64_t *faults;  /* [1]  rows whose solver failed                         */
-    double *bucket;   /* [mq_bucket_slots() * bcap] column-sum buckets (scratch) */
+    double *bucket;   /* column-sum scratch: mq_bucket_slots() * bcap doubles
+                         (bucket mode) or m u64 accumulators (fixed-point mode,
+                         zero between iterations)                              */
     double *srow;     /* [n] [pad] per-buyer utility after the last prox: the
                          row solve's warm start (<= 0: none; any value is
                          correct, a close one saves sweeps)                    */
@@ -227,8 +234,10 @@ int64_t mq_scratch_doubles(void);
 
 const char *mq_last_error(void);
 int mq_abi_version(void);
-/* rotating column-sum buckets the default build needs (0: none) */
+/* rotating column-sum buckets the build needs (0: none) */
 int mq_bucket_slots(void);
+/* 1 if the build sums columns in fixed point (state.bucket = m u64) */
+int mq_fixed_colsum(void);
 
 #ifdef __cplusplus
 }

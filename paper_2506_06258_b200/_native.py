@@ -17,7 +17,7 @@ TILE_ENTRIES = 2816   # MQ_TILE_ENTRIES
 LONG_ROW = 1024       # MQ_LONG_ROW
 TILE_ROWS = 256       # MQ_TILE_ROWS
 PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _lock = threading.Lock()
 _lib = None
@@ -42,7 +42,8 @@ class MqMarket(ctypes.Structure):
                 ("tiles", P), ("ntiles", I64), ("long_rows", P), ("nlong", I64),
                 ("bperm", P), ("bptr", P), ("nblk", I64), ("tiles_per_block", I64),
                 ("prim_grid", ctypes.c_int32), ("tpos", P), ("tptr", P), ("row_begin", I64),
-                ("bpos", P), ("bcap", I64)]
+                ("bpos", P), ("bcap", I64), ("cs_scale", ctypes.c_double),
+                ("cs_xmax", ctypes.c_double)]
 
 
 class MqState(ctypes.Structure):
@@ -79,6 +80,7 @@ _SIGS = {
     "mq_last_error": (ctypes.c_char_p, []),
     "mq_abi_version": (CINT, []),
     "mq_bucket_slots": (CINT, []),
+    "mq_fixed_colsum": (CINT, []),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -29,11 +29,25 @@
 #ifndef MQ_G
 #define MQ_G 16
 #endif
+// column-sum mode: default = sparse fixed-point atomics (no column-sum warps);
+// the gather / scatter / bucket modes are kept as measured alternatives
+#if defined(MQ_CS_GATHER) || defined(MQ_SCATTER) || defined(MQ_COLSUM_SPLIT) || \
+    defined(MQ_COLSUM_PHASED) || defined(MQ_CS_BUCKET)
+#define MQ_CS_DENSE 1
+#endif
 #ifndef MQ_NCW
+#ifdef MQ_CS_DENSE
 #define MQ_NCW 4
+#else
+#define MQ_NCW 0
+#endif
 #endif
 #ifndef MQ_NSW
+#ifdef MQ_CS_DENSE
 #define MQ_NSW 15
+#else
+#define MQ_NSW 19  /* no column-sum warps: 20 warps at 96 registers */
+#endif
 #endif
 #ifndef MQ_NGW
 #define MQ_NGW 0
@@ -182,6 +196,23 @@ __device__ __forceinline__ double ld_price(const double *a) {
 #else
     return __ldg(a);
 #endif
+}
+
+// Column sums as fixed-point integers: x_e * cs_scale rounded to u64, added
+// with fire-and-forget atomics only for the ~1 % of entries with x_e > 0.
+// Integer addition is associative, so the sums are bitwise deterministic in
+// any order; cs_scale = 2^e is chosen per market so that no column can
+// overflow while every x_e < cs_xmax (a larger x_e is counted as a fault).
+__device__ __forceinline__ void fixed_colsum_add(const mq_market &mk, const mq_state &st, int j,
+                                                 double xe) {
+    if (xe < mk.cs_xmax) {
+        asm volatile("red.global.add.u64 [%0], %1;" ::"l"(reinterpret_cast<unsigned long long *>(
+                         st.bucket) + j),
+                     "l"(__double2ull_rn(xe * mk.cs_scale))
+                     : "memory");
+    } else {
+        atomicAdd(reinterpret_cast<unsigned long long *>(st.faults), 1ull);
+    }
 }
 
 // ------------------------------------------------------------ price step
@@ -432,10 +463,10 @@ constexpr bool kScatter = true;       // column sums from a column-major copy of
 #else
 constexpr bool kScatter = false;
 #endif
-#ifdef MQ_CS_ATOMIC
-constexpr bool kAtomic = true;        // experiment: fixed-point integer atomics per entry
-#else
+#ifdef MQ_CS_DENSE
 constexpr bool kAtomic = false;
+#else
+constexpr bool kAtomic = true;        // sparse fixed-point column sums (default)
 #endif
 #ifdef MQ_CS_BUCKET
 constexpr bool kBucket = !kScatter;   // solvers store x into L2 buckets in column order
@@ -665,7 +696,7 @@ template <int G, int NSW, int NGW, int NCW, int ETILE, int RTILE, int NSTAGE, in
 __global__ void __launch_bounds__((NSW + NGW + NCW + 1) * 32, 1)
 primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
                     int write_cs, int64_t tile_lo, int64_t tile_hi, int *tile_ctr) {
-    using L = TileLayout<ETILE, RTILE, (NGW > 0)>;
+    using L = TileLayout<ETILE, RTILE, false>;  // c (gather warps) is written over x
     MQ_PROF_DECL();
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTAGE * L::kStage);
@@ -864,10 +895,12 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 const int64_t e0 = srp[0];
                 const int cnt = (int)(srp[nrows] - e0);
                 const int d8 = (int)(((e0 * 8) & 15) >> 3), d4 = (int)(((e0 * 4) & 15) >> 2);
-                const double *sx = reinterpret_cast<const double *>(base + L::kX) + d8;
-                double *sc = reinterpret_cast<double *>(base + L::kC) + d8;
+                // c = x - tau p[col] replaces x in the stage (the solvers read
+                // c and the warm start srow; x itself is not needed again)
+                double *sx = reinterpret_cast<double *>(base + L::kX) + d8;
+                double *sc = sx;
                 const int32_t *scol = reinterpret_cast<const int32_t *>(base + L::kCol) + d4;
-                constexpr int U = 4;
+                constexpr int U = 8;
                 for (int t0 = gt; t0 < cnt; t0 += NGW * 32 * U) {
                     double pv[U];
 #pragma unroll
@@ -886,6 +919,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     }
                 }
             }
+            fence_proxy_async();  // generic writes before the stage's next bulk refill
             __syncwarp();
             if (wl == 0) mbar_arrive(&ready[s]);
             if (k < 0) break;
@@ -1359,7 +1393,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         // c = x - tau p[col]: from the gather warps, or computed here (then
         // written over x in place for the shared-memory path)
         double *sc = kXDirect ? st.x + e0
-                              : reinterpret_cast<double *>(base + (NGW > 0 ? L::kC : L::kX)) + d8;
+                              : reinterpret_cast<double *>(base + L::kX) + d8;
         auto ldx = [&](int t) -> double { return kXDirect ? ld_na(st.x + e0 + t) : sx[t]; };
         auto ldxb = [&](int t) -> double { return kXBDirect ? ld_na(st.xbar + e0 + t) : sxb[t]; };
         const int32_t *scol = reinterpret_cast<const int32_t *>(base + L::kCol) + d4;
@@ -1395,9 +1429,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     __stcs(st.xbar + e0 + t, av.wold * ldxb(t) + av.wnew * xn);
                     if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
                     if (kBucket) st_keep(bslot + stp[t], xn, pkeep);
-                    if (kAtomic)
-                        atomicAdd(reinterpret_cast<unsigned long long *>(st.bucket) + scol[t],
-                                  (unsigned long long)__double2ll_rn(xn * 0x1p40));
+                    if (kAtomic && xn > 0.0) fixed_colsum_add(mk, st, scol[t], xn);
                 }
             }
             if (false) {
@@ -1465,9 +1497,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                         __stcs(st.xbar + e0 + t, av.wold * (kXBDirect ? xb[e % XP] : ldxb(t)) + av.wnew * xn);
                         if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
                     if (kBucket) st_keep(bslot + stp[t], xn, pkeep);
-                    if (kAtomic)
-                        atomicAdd(reinterpret_cast<unsigned long long *>(st.bucket) + scol[t],
-                                  (unsigned long long)__double2ll_rn(xn * 0x1p40));
+                    if (kAtomic && xn > 0.0) fixed_colsum_add(mk, st, scol[t], xn);
                     }
                 }
                 MQ_TS(tq3);
@@ -1491,7 +1521,8 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     ap += ue * ce;
                     bp += ue * ue;
                 }
-                const double s0 = group_sum<G>(s0p);
+                // with gather warps x is gone from the stage: warm start from srow
+                const double s0 = NGW > 0 ? (has ? ss[r] : 0.0) : group_sum<G>(s0p);
                 const double A = group_sum<G>(ap);
                 const double B = group_sum<G>(bp);
                 const double sr =
@@ -1504,9 +1535,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     __stcs(st.xbar + e0 + t, av.wold * ldxb(t) + av.wnew * xn);
                     if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
                     if (kBucket) st_keep(bslot + stp[t], xn, pkeep);
-                    if (kAtomic)
-                        atomicAdd(reinterpret_cast<unsigned long long *>(st.bucket) + scol[t],
-                                  (unsigned long long)__double2ll_rn(xn * 0x1p40));
+                    if (kAtomic && xn > 0.0) fixed_colsum_add(mk, st, scol[t], xn);
                 }
                 // c was written over x in this stage: order those generic-proxy
                 // writes before the producer's next bulk copy into the stage
@@ -1526,7 +1555,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
                          : "=r"(prior) : "r"(smem_addr(&claim[NSTAGE + s])) : "memory");
 #ifndef MQ_NO_PUBLISH
-            if (!kSplit && !kScatter && !kPhased && prior == NSW - 1) {
+            if (!kSplit && !kScatter && !kPhased && !kAtomic && prior == NSW - 1) {
                 __threadfence();
                 atomicAdd(&st.blk_done[k / tpb_all], 1);
             }
@@ -1658,6 +1687,7 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
             st.x[t] = xn;
             st.xbar[t] = av.wold * st.xbar[t] + av.wnew * xn;
             if (kScatter) st.xc[mk.tpos[t]] = xn;
+            if (kAtomic && xn > 0.0) fixed_colsum_add(mk, st, mk.col[t], xn);
         }
         __syncthreads();
     }
@@ -1792,9 +1822,9 @@ constexpr int kEtile = MQ_ETILE;
 #ifdef MQ_CS_PERWARP
 constexpr int kQMax = (kWCols + 31) / 32;  // goods per column-sum lane
 #else
-constexpr int kQMax = (1152 + kNCW * 32 - 1) / (kNCW * 32);  // goods per column-sum thread
+constexpr int kQMax = kNCW > 0 ? (1152 + kNCW * 32 - 1) / (kNCW * 32) : 1;  // goods per thread
 #endif
-using PrimalLayout = TileLayout<kEtile, MQ_TILE_ROWS, (kNGW > 0)>;
+using PrimalLayout = TileLayout<kEtile, MQ_TILE_ROWS, false>;
 
 constexpr int kPrimalSmem = MQ_SMEM_PAD + kStages * PrimalLayout::kStage + 7 * kStages * 8 + 4 * kStages * 4 + 128 +
                             (kPhased ? kPhChunk * 8 : (kScatter || kSplit) ? 0 :
@@ -1802,8 +1832,9 @@ constexpr int kPrimalSmem = MQ_SMEM_PAD + kStages * PrimalLayout::kStage + 7 * k
                              kNCW * (((2 * (kCsChunk + 8) + 2 * (kWCols + 8)) * 4 + kCsChunk * 8 +
                                       8 * 8 + 2 * 8 + 127) / 128 * 128)
 #else
-                             kBucket ? (kCsCols + 8) * 4 + 2 * (kBkChunk + 4) * 8 + 3 * 8 + 16
-                                     : (kCsCap + kCsCols + 8) * 4 + 4 * 8 + 16
+                             kAtomic ? 0
+                             : kBucket ? (kCsCols + 8) * 4 + 2 * (kBkChunk + 4) * 8 + 3 * 8 + 16
+                                       : (kCsCap + kCsCols + 8) * 4 + 4 * 8 + 16
 #endif
                             );
 
@@ -1853,19 +1884,27 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
 }
 
 // adds the long rows (pseudo-block nblk) to cs; csbar update when finalize
-__global__ void cs_from_fixed_kernel(int64_t m, unsigned long long *fix, double *cs) {
+__global__ void cs_from_fixed_kernel(int64_t m, unsigned long long *__restrict__ fix,
+                                     double *__restrict__ cs, double *__restrict__ csbar,
+                                     const int64_t *__restrict__ navg, int it, double inv_scale) {
+    const Avg av = avg_weights(navg, it);
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
          j += (int64_t)gridDim.x * blockDim.x) {
-        cs[j] = (double)(long long)fix[j] * 0x1p-40;
+        const double c = (double)fix[j] * inv_scale;  // exact for sums < 2^53 units
+        cs[j] = c;
         fix[j] = 0ull;
+        if (csbar) csbar[j] = av.wold * csbar[j] + av.wnew * c;
     }
 }
 
 int colsum_rest_launch(const mq_market *mk, const mq_state *st, int it, int finalize,
                        cudaStream_t s) {
-    if (kAtomic)
+    if (kAtomic) {  // every entry (tiles and long rows) went through the atomics
         cs_from_fixed_kernel<<<grid_for(mk->m, 256, sm_count() * 8), 256, 0, s>>>(
-            mk->m, reinterpret_cast<unsigned long long *>(st->bucket), st->cs);
+            mk->m, reinterpret_cast<unsigned long long *>(st->bucket), st->cs,
+            finalize ? st->csbar : nullptr, st->navg, it, 1.0 / mk->cs_scale);
+        return check_launch("mq_colsum_step");
+    }
     if (kScatter) {
         colsum_xc_kernel<<<grid_for(mk->m, 8, sm_count() * 8), 256, 0, s>>>(
             mk->m, mk->tptr, st->xc, st->cs, finalize ? st->csbar : nullptr, st->navg, it);
@@ -1944,7 +1983,9 @@ int mq_debug_counters(unsigned long long *out_host) {
 
 int mq_tile_entries(void) { return kEtile; }
 
-int mq_colsum_mode(void) { return kScatter ? 1 : (kSplit ? 2 : (kPhased ? 3 : (kBucket ? 4 : 0))); }
+int mq_colsum_mode(void) {
+    return kScatter ? 1 : (kSplit ? 2 : (kPhased ? 3 : (kBucket ? 4 : (kAtomic ? 5 : 0))));
+}
 
 int mq_bucket_slots(void) { return kBucket ? (int)kLag : 0; }
 int mq_fixed_colsum(void) { return kAtomic ? 1 : 0; }

@@ -16,6 +16,7 @@ Built once per instance (or per row shard); every later call only passes the
 `mq_market` struct of raw pointers to the native library.
 """
 
+import math
 import os
 import ctypes
 import warnings
@@ -174,6 +175,15 @@ def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
     return bperm[:nnz], bptr32[:total + 1], nblk, tpb, bpos, bcap
 
 
+def fixed_point_scale(max_col_count):
+    """(cs_scale, cs_xmax) of the fixed-point column sums: cs_scale = 2^k,
+    2^-48 <= resolution <= 2^-24, aiming at cs_xmax ~ 1024, with
+    cs_xmax * cs_scale * max_col_count = 2^62 (no u64 overflow)."""
+    c = max(1, int(max_col_count))
+    k = int(min(48, max(24, math.floor(62 - math.log2(c) - 10))))
+    return float(2.0 ** k), float(2.0 ** (62 - k) / c)
+
+
 class DeviceMarket:
     """CSR utilities + budgets on one GPU (optionally a row shard).
 
@@ -236,6 +246,7 @@ class DeviceMarket:
                 self.row_ptr, self.col, self.m, tiles2, self.long_rows, self.prim_grid,
                 tiles_per_block=SPLIT_TILES_PER_BLOCK if mode in (2, 3) else None,
                 with_bpos=mode == 4)
+            self.max_col_count = int(self.col_counts.max().item()) if self.m else 0
             lens = self.row_ptr[1:] - self.row_ptr[:-1]
             self.max_row_len = int(lens.max().item()) if self.n else 0
         self.tperm = self.tptr = None
@@ -281,6 +292,7 @@ class DeviceMarket:
         if self._bpos is not None:
             s.bpos = self._bpos.data_ptr()
         s.bcap = int(self.bcap)
+        s.cs_scale, s.cs_xmax = fixed_point_scale(self.max_col_count)
         return s
 
     @classmethod
