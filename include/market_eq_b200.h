@@ -32,8 +32,8 @@
 extern "C" {
 #endif
 
-#define MQ_ABI_VERSION 3
-#define MQ_TILE_ENTRIES 2816 /* entries staged per shared-memory tile (default build) */
+#define MQ_ABI_VERSION 4
+#define MQ_TILE_ENTRIES 3584 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
 
@@ -113,6 +113,13 @@ typedef struct mq_state {
     double *srow;     /* [n] [pad] per-buyer utility after the last prox: the
                          row solve's warm start (<= 0: none; any value is
                          correct, a close one saves sweeps)                    */
+    /* sparse iterate (mq_x_sparse() == 1): xflag[e] = (x[e] > 0) is staged
+       instead of x (x is read only where flagged and stays exact); xsum =
+       sum of x since the last restart, xbar = xsum / navg is written by
+       mq_avg_materialize.  The host sets xflag = 1 and xsum = navg * xbar
+       whenever it writes x, xbar or navg itself.                            */
+    uint8_t *xflag;   /* [nnz] [pad]                                          */
+    double *xsum;     /* [nnz]                                                */
 } mq_state;
 
 /* ---- faithful drop-in ------------------------------------------------------
@@ -238,6 +245,10 @@ int mq_abi_version(void);
 int mq_bucket_slots(void);
 /* 1 if the build sums columns in fixed point (state.bucket = m u64) */
 int mq_fixed_colsum(void);
+/* 1 if the build keeps the sparse iterate (xflag / xsum) */
+int mq_x_sparse(void);
+/* sparse iterate: xbar = xsum / navg (call after mq_chunk_end) */
+int mq_avg_materialize(const mq_market *mk, const mq_state *st, void *stream);
 
 #ifdef __cplusplus
 }

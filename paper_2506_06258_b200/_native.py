@@ -13,11 +13,11 @@ from .errors import MarketError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MQ_LIB") or os.path.join(_PKG, "libmarket_eq_b200.so")
-TILE_ENTRIES = 2816   # MQ_TILE_ENTRIES
+TILE_ENTRIES = 3584   # MQ_TILE_ENTRIES
 LONG_ROW = 1024       # MQ_LONG_ROW
 TILE_ROWS = 256       # MQ_TILE_ROWS
 PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _lock = threading.Lock()
 _lib = None
@@ -49,7 +49,8 @@ class MqMarket(ctypes.Structure):
 class MqState(ctypes.Structure):
     _fields_ = [("x", P), ("xbar", P), ("p", P), ("pbar", P), ("cs", P), ("cs_prev", P),
                 ("csbar", P), ("blk_done", P), ("xc", P), ("steps", P), ("navg", P),
-                ("pass_out", P), ("faults", P), ("bucket", P), ("srow", P)]
+                ("pass_out", P), ("faults", P), ("bucket", P), ("srow", P),
+                ("xflag", P), ("xsum", P)]
 
 
 PM = ctypes.POINTER(MqMarket)
@@ -81,6 +82,8 @@ _SIGS = {
     "mq_abi_version": (CINT, []),
     "mq_bucket_slots": (CINT, []),
     "mq_fixed_colsum": (CINT, []),
+    "mq_x_sparse": (CINT, []),
+    "mq_avg_materialize": (CINT, [PM, PS, P]),
 }
 
 EXPORTED = tuple(_SIGS)

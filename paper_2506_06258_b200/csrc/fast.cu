@@ -60,7 +60,11 @@
 #define MQ_ETILE MQ_TILE_ENTRIES
 #endif
 #ifndef MQ_STAGES
+#if defined(MQ_CS_DENSE) || defined(MQ_X_DENSE)
 #define MQ_STAGES 2
+#else
+#define MQ_STAGES 3  /* sparse iterate: 13 B/entry stages, 3 fit with 92 KB of L1 */
+#endif
 #endif
 #ifndef MQ_LAG
 #define MQ_LAG 4
@@ -169,6 +173,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 #endif
 }
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
                                          uint64_t *bar) {
     asm volatile(
@@ -189,6 +201,9 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // price gather p[col]: read-only, L2-resident (m * 8 bytes); optionally kept
 // out of L1 so the gathers do not evict the warps' other L1 lines
 __device__ __forceinline__ double ld_price(const double *a) {
+#ifdef MQ_EXP_NOP  // timing experiment only (wrong results): no price gathers
+    return 1e-3 * (double)(reinterpret_cast<uintptr_t>(a) & 7);
+#endif
 #ifdef MQ_P_NOALLOC
     double v;
     asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(a));
@@ -484,17 +499,37 @@ constexpr bool kPhased = true;        // solve a block of tiles, grid barrier, g
 constexpr bool kPhased = false;       // default: column-sum warps gather concurrently (fused)
 #endif
 constexpr int kPhChunk = 4096;
+// Sparse iterate (default with the fixed-point column sums): ~99 % of x is 0
+// after the first iteration, so x is not streamed.  A byte flag per entry
+// (x > 0) is staged instead; only flagged entries load their x, x is written
+// only where it is or was nonzero, and the running average is kept as the
+// running sum S = sum of x since the restart (atomic adds on nonzero x only),
+// materialized as xbar = S / count once per chunk (mq_avg_materialize).
+#if !defined(MQ_CS_DENSE) && !defined(MQ_X_DENSE)
+constexpr bool kSparse = true;
+#else
+constexpr bool kSparse = false;
+#endif
 #ifdef MQ_X_DIRECT
 constexpr bool kXDirect = true;   // x is L2-prefetched and loaded by the solvers, not staged
 #else
-constexpr bool kXDirect = false;
+constexpr bool kXDirect = kSparse;
+#endif
+// software-pipelined solver warps (sparse iterate only): measured slower (a
+// warp holds two tiles' stages, so fewer tiles are in flight); opt-in
+#if defined(MQ_PIPE) && !defined(MQ_CS_DENSE) && !defined(MQ_X_DENSE) && \
+    !defined(MQ_TRIVIAL_SOLVE) && (MQ_NGW == 0)
+constexpr bool kPipe = true;
+#else
+constexpr bool kPipe = false;
 #endif
 #ifdef MQ_XB_DIRECT
 constexpr bool kXBDirect = true;  // xbar likewise
 #else
-constexpr bool kXBDirect = false;
+constexpr bool kXBDirect = kSparse;
 #endif
-static_assert(!(kXDirect || kXBDirect) || (MQ_NGW == 0 && !kPhased && !kScatter && !kSplit),
+static_assert(!kSparse || kAtomic, "the sparse iterate needs the fixed-point column sums");
+static_assert(!(kXDirect || kXBDirect) || ((MQ_NGW == 0 || kSparse) && !kPhased && !kScatter && !kSplit),
               "direct x/xbar loads: default (fused) mode only");        // gathered values staged per round (phased mode)
 
 template <int ETILE, int RTILE, bool HASC>
@@ -511,8 +546,10 @@ struct TileLayout {
     static constexpr int kRp = kTp + ((kScatter || kBucket) ? (ETILE + 4) * 4 : 0);
     static constexpr int kW = kRp + (RTILE + 4) * 8;
     static constexpr int kS = kW + (RTILE + 2) * 8;  // srow: warm-start utilities
-    static constexpr int kStage = (kS + (RTILE + 2) * 8 + 127) / 128 * 128;
-    static_assert(kX % 16 == 0 && kCol % 16 == 0 && kRp % 16 == 0 && kW % 16 == 0 && kS % 16 == 0,
+    static constexpr int kF = kS + (RTILE + 2) * 8;  // x > 0 flags (sparse iterate), u8
+    static constexpr int kStage = (kF + (kSparse ? ETILE + 32 : 0) + 127) / 128 * 128;
+    static_assert(kX % 16 == 0 && kCol % 16 == 0 && kRp % 16 == 0 && kW % 16 == 0 && kS % 16 == 0 &&
+                      kF % 16 == 0,
                   "bulk-copy destinations must be 16-byte aligned");
 };
 
@@ -540,6 +577,14 @@ __device__ __forceinline__ double ld_na(const double *a) {
     double v;
     asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(a) : "memory");
     return v;
+}
+__device__ __forceinline__ void st_flag(uint8_t *p, bool v) {
+    asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"((int)v) : "memory");
+}
+// fire-and-forget float add (one writer per address and iteration: the
+// result is the plain rounded sum, deterministic)
+__device__ __forceinline__ void red_add_f64(double *p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
@@ -696,7 +741,9 @@ template <int G, int NSW, int NGW, int NCW, int ETILE, int RTILE, int NSTAGE, in
 __global__ void __launch_bounds__((NSW + NGW + NCW + 1) * 32, 1)
 primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
                     int write_cs, int64_t tile_lo, int64_t tile_hi, int *tile_ctr) {
-    using L = TileLayout<ETILE, RTILE, false>;  // c (gather warps) is written over x
+    // c (gather warps) is written over the staged x, or into its own region
+    // when x is not staged (sparse iterate)
+    using L = TileLayout<ETILE, RTILE, (NGW > 0 && kXDirect)>;
     MQ_PROF_DECL();
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + NSTAGE * L::kStage);
@@ -859,16 +906,22 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 constexpr int n8 = 1 + (kXDirect ? 0 : 1) + (kXBDirect ? 0 : 1);
                 const unsigned char *src_s;
                 aligned_span<8>(st.srow, r0, r1 - r0, &src_s, &bw);
+                const unsigned char *src_f = nullptr;
+                uint32_t b1 = 0;
+                if (kSparse) aligned_span<1>(st.xflag, e0, cnt, &src_f, &b1);
                 mbar_expect_tx(&full[s], brp + 2 * bw +
-                                             (cnt > 0 ? n8 * b8 + ((kScatter || kBucket) ? 2 : 1) * b4 : 0));
+                                             (cnt > 0 ? n8 * b8 + ((kScatter || kBucket) ? 2 : 1) * b4 + b1
+                                                      : 0));
                 bulk_g2s(base + L::kRp, src_rp, brp, &full[s]);
                 bulk_g2s(base + L::kW, src_w, bw, &full[s]);
                 bulk_g2s(base + L::kS, src_s, bw, &full[s]);
                 if (cnt > 0) {
                     bulk_g2s_hint(base + L::kU, src_u, b8, &full[s], pol);
-                    if (kXDirect) prefetch_l2(src_x, b8);
+                    if (kSparse) bulk_g2s_hint(base + L::kF, src_f, b1, &full[s], pol);
+                    else if (kXDirect) prefetch_l2(src_x, b8);
                     else bulk_g2s(base + L::kX, src_x, b8, &full[s]);
-                    if (kXBDirect) prefetch_l2(src_xb, b8);
+                    if (kSparse) {
+                    } else if (kXBDirect) prefetch_l2(src_xb, b8);
                     else bulk_g2s_hint(base + L::kXB, src_xb, b8, &full[s], pol);
                     bulk_g2s_hint(base + L::kCol, src_c, b4, &full[s], pol);
                     if (kScatter || kBucket) bulk_g2s_hint(base + L::kTp, src_tp, b4, &full[s], pol);
@@ -898,8 +951,9 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 // c = x - tau p[col] replaces x in the stage (the solvers read
                 // c and the warm start srow; x itself is not needed again)
                 double *sx = reinterpret_cast<double *>(base + L::kX) + d8;
-                double *sc = sx;
+                double *sc = kXDirect ? reinterpret_cast<double *>(base + L::kC) + d8 : sx;
                 const int32_t *scol = reinterpret_cast<const int32_t *>(base + L::kCol) + d4;
+                const uint8_t *sfl = reinterpret_cast<const uint8_t *>(base + L::kF) + (int)(e0 & 15);
                 constexpr int U = 8;
                 for (int t0 = gt; t0 < cnt; t0 += NGW * 32 * U) {
                     double pv[U];
@@ -912,7 +966,9 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     for (int q = 0; q < U; ++q) {
                         const int t = t0 + q * NGW * 32;
                         if (t < cnt) {
-                            const double xe = sx[t];
+                            const double xe = !kXDirect ? sx[t]
+                                              : kSparse ? (sfl[t] ? ld_na(st.x + e0 + t) : 0.0)
+                                                        : ld_na(st.x + e0 + t);
                             sc[t] = xe - tau * pv[q];
                             if (x_prev_out) x_prev_out[e0 + t] = xe;
                         }
@@ -1349,7 +1405,212 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
     int my_sweeps = 0;  // per warp and launch: < 2^31
     int my_faults = 0;
     int64_t ph_blk = 0;
-    for (int64_t j = 0;; ++j) {
+    if (kPipe) {
+        // Software-pipelined solver: while a warp solves its current row
+        // pair, the price gathers of its next pair (claimed ahead, possibly
+        // from the next tile) are already in flight.  A warp leaves a tile
+        // (arrives on empty[s]) once a claim there fails and the pair it still
+        // holds from that tile is done.
+        constexpr int RP = kRegPer;
+        int64_t jt = -1;
+        int ts = 0, tn = 0;  // stage / rows of the tile being claimed from
+        bool tile_ok = false;
+        auto enter_tile = [&]() {
+            ++jt;
+            ts = (int)(jt % NSTAGE);
+            mbar_wait(&full[ts], (uint32_t)((jt / NSTAGE) & 1));
+            tile_ok = stile[ts] >= 0;
+            tn = tile_ok ? (int)(smeta[3 * ts + 1] - smeta[3 * ts]) : 0;
+        };
+        auto leave = [&](int s_) {
+            __syncwarp();
+            if (wl == 0) mbar_arrive(&empty[s_]);
+        };
+        struct View {  // a staged tile's arrays
+            int64_t r0, e0;
+            int nrows;
+            const int64_t *srp;
+            const double *sw, *ss, *su;
+            const int32_t *scol;
+            const uint8_t *sfl;
+        };
+        auto view = [&](int s_) {
+            View v;
+            v.r0 = smeta[3 * s_];
+            v.nrows = (int)(smeta[3 * s_ + 1] - v.r0);
+            unsigned char *b_ = smem + s_ * L::kStage;
+            const int lr = (int)(((v.r0 * 8) & 15) >> 3);
+            v.srp = reinterpret_cast<const int64_t *>(b_ + L::kRp) + lr;
+            v.sw = reinterpret_cast<const double *>(b_ + L::kW) + lr;
+            v.ss = reinterpret_cast<const double *>(b_ + L::kS) + lr;
+            v.e0 = v.srp[0];
+            v.su = reinterpret_cast<const double *>(b_ + L::kU) + (int)(((v.e0 * 8) & 15) >> 3);
+            v.scol = reinterpret_cast<const int32_t *>(b_ + L::kCol) + (int)(((v.e0 * 4) & 15) >> 2);
+            v.sfl = reinterpret_cast<const uint8_t *>(b_ + L::kF) + (int)(v.e0 & 15);
+            return v;
+        };
+        int cur_s = -1, defer = -1;
+        int nx_s = -1, nx_rb = 0;
+        bool nx_reg = false, blocked = false;
+        double pn[RP];
+        auto claim_next = [&]() {
+            nx_s = -1;
+            while (tile_ok) {
+                int rb = 0;
+                if (wl == 0) rb = atomicAdd(&claim[ts], GPW);
+                rb = __shfl_sync(MQ_FULL, rb, 0);
+                if (rb < tn) {
+                    nx_s = ts;
+                    nx_rb = rb;
+                    return;
+                }
+                if (cur_s == ts) defer = ts;  // its last pair here is still running
+                else leave(ts);
+                // the next tile would reuse the stage this warp still holds:
+                // claim again once the current pair is done (no deadlock)
+                // nor wait for a tile still loading while a pair is in hand
+                const int64_t jn = jt + 1;
+                // one lane's view of the barrier, so the warp stays converged
+                const bool loaded = __shfl_sync(
+                    MQ_FULL, (int)mbar_test(&full[(int)(jn % NSTAGE)], (uint32_t)((jn / NSTAGE) & 1)), 0);
+                if (cur_s >= 0 && ((defer >= 0 && (int)(jn % NSTAGE) == defer) || !loaded)) {
+                    blocked = true;
+                    return;
+                }
+                enter_tile();
+            }
+        };
+        auto issue_next = [&]() {  // the next pair's price gathers
+            nx_reg = false;
+            if (nx_s < 0) return;
+            const View v = view(nx_s);
+            const int r = nx_rb + gsub;
+            int a = 0, b = 0;
+            if (r < v.nrows) {
+                a = (int)(v.srp[r] - v.e0);
+                b = (int)(v.srp[r + 1] - v.e0);
+            }
+            nx_reg = __all_sync(MQ_FULL, b - a <= RP * G);
+            if (nx_reg) {
+#pragma unroll
+                for (int e = 0; e < RP; ++e) {
+                    const int t = a + lane + e * G;
+                    pn[e] = t < b ? ld_price(st.p + v.scol[t]) : 0.0;
+                }
+            }
+        };
+        enter_tile();
+        claim_next();
+        issue_next();
+        while (nx_s >= 0) {
+            const int cs_ = nx_s, crb = nx_rb;
+            const bool creg = nx_reg;
+            double pv[RP];
+#pragma unroll
+            for (int e = 0; e < RP; ++e) pv[e] = pn[e];
+            cur_s = cs_;
+            claim_next();
+            issue_next();
+            // ---- solve the current pair
+            const View v = view(cs_);
+            const int r = crb + gsub;
+            const bool has = r < v.nrows;
+            int a = 0, b = 0;
+            double tw = 0.0;
+            if (has) {
+                a = (int)(v.srp[r] - v.e0);
+                b = (int)(v.srp[r + 1] - v.e0);
+                tw = tau * v.sw[r];
+            }
+            const int64_t e0 = v.e0;
+            int nsw = 0;
+            bool ok = true;
+            if (creg) {
+                double c[RP];
+                uint32_t fb = 0;
+#pragma unroll
+                for (int e = 0; e < RP; ++e) {
+                    const int t = a + lane + e * G;
+                    c[e] = 0.0;
+                    if (t < b) {
+                        const bool f = v.sfl[t] != 0;
+                        if (f) fb |= 1u << e;
+                        const double xe = f ? ld_na(st.x + e0 + t) : 0.0;
+                        if (x_prev_out) x_prev_out[e0 + t] = xe;
+                        c[e] = xe - tau * pv[e];
+                    }
+                }
+                const double s0 = has ? v.ss[r] : 0.0;
+                const uint32_t gmask = G == 32 ? MQ_FULL : (((1u << G) - 1u) << (gsub * G));
+                const uint32_t su_l = smem_addr(v.su + a + lane);
+                const int n_l = b - a - lane > 0 ? (b - a - lane + G - 1) / G : 0;
+                auto uf = [&](int e) -> double { return e < n_l ? lds_f64(su_l + e * G * 8) : 0.0; };
+                const double sr = row_root_warm<G, RP>(c, uf, tw, s0, has, gmask, &nsw, &ok);
+                if (has && lane == 0) st.srow[v.r0 + r] = sr;
+                const double inv_s = 1.0 / sr;
+#pragma unroll
+                for (int e = 0; e < RP; ++e) {
+                    const int t = a + lane + e * G;
+                    if (t < b) {
+                        const double xn = fmax(c[e] + tw * v.su[t] * inv_s, 0.0);
+                        const bool nz = xn > 0.0;
+                        st_flag(st.xflag + e0 + t, nz);
+                        if (nz || ((fb >> e) & 1u)) st.x[e0 + t] = xn;
+                        if (nz) {
+                            red_add_f64(st.xsum + e0 + t, xn);
+                            fixed_colsum_add(mk, st, v.scol[t], xn);
+                        }
+                    }
+                }
+            } else {
+                // longer rows: c is kept in x (global) across the sweeps
+                double *sc = st.x + e0;
+                double ap = 0.0, bp = 0.0;
+                for (int t = a + lane; t < b; t += G) {
+                    const double ue = v.su[t];
+                    const double xe = v.sfl[t] ? ld_na(st.x + e0 + t) : 0.0;
+                    if (x_prev_out) x_prev_out[e0 + t] = xe;
+                    const double ce = xe - tau * ld_price(st.p + v.scol[t]);
+                    sc[t] = ce;
+                    ap += ue * ce;
+                    bp += ue * ue;
+                }
+                const double s0 = has ? v.ss[r] : 0.0;
+                const double A = group_sum<G>(ap);
+                const double B = group_sum<G>(bp);
+                const double sr =
+                    row_root_exact<G>(v.su, sc, a, b, lane, tw, s0, A, B, has, &nsw, &ok);
+                if (has && lane == 0) st.srow[v.r0 + r] = sr;
+                const double inv_s = 1.0 / sr;
+                for (int t = a + lane; t < b; t += G) {
+                    const double xn = fmax(sc[t] + tw * v.su[t] * inv_s, 0.0);
+                    const bool nz = xn > 0.0;
+                    st_flag(st.xflag + e0 + t, nz);
+                    st.x[e0 + t] = xn;
+                    if (nz) {
+                        red_add_f64(st.xsum + e0 + t, xn);
+                        fixed_colsum_add(mk, st, v.scol[t], xn);
+                    }
+                }
+            }
+            if (has && b > a && lane == 0) {
+                my_sweeps += nsw;
+                if (!ok) ++my_faults;
+            }
+            cur_s = -1;
+            if (defer == cs_) {
+                leave(cs_);
+                defer = -1;
+            }
+            if (blocked) {
+                blocked = false;
+                enter_tile();
+                claim_next();
+                issue_next();
+            }
+        }
+    }
+    for (int64_t j = 0; !kPipe; ++j) {
         const int s = (int)(j % NSTAGE);
         {
             MQ_T0();
@@ -1392,13 +1653,33 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         const double *sxb = reinterpret_cast<const double *>(base + L::kXB) + d8;
         // c = x - tau p[col]: from the gather warps, or computed here (then
         // written over x in place for the shared-memory path)
-        double *sc = kXDirect ? st.x + e0
-                              : reinterpret_cast<double *>(base + L::kX) + d8;
+        double *sc = (NGW > 0 && kXDirect) ? reinterpret_cast<double *>(base + L::kC) + d8
+                     : kXDirect ? st.x + e0
+                                : reinterpret_cast<double *>(base + L::kX) + d8;
         auto ldx = [&](int t) -> double { return kXDirect ? ld_na(st.x + e0 + t) : sx[t]; };
         auto ldxb = [&](int t) -> double { return kXBDirect ? ld_na(st.xbar + e0 + t) : sxb[t]; };
         const int32_t *scol = reinterpret_cast<const int32_t *>(base + L::kCol) + d4;
         const int32_t *stp = reinterpret_cast<const int32_t *>(base + L::kTp) + d4;
         double *bslot = kBucket ? st.bucket + (blk % kLag) * mk.bcap : nullptr;
+        const uint8_t *sfl = reinterpret_cast<const uint8_t *>(base + L::kF) + (int)(e0 & 15);
+        // sparse iterate: x of flagged entries only, zero otherwise
+        auto ldxs = [&](int t) -> double {
+#ifdef MQ_EXP_NOX  // timing experiment only (wrong results): no x loads
+            return 0.0 * sfl[t];
+#endif
+            return kSparse ? (sfl[t] ? ld_na(st.x + e0 + t) : 0.0) : ldx(t);
+        };
+        // store x^{k+1} (+ its flag and running sum, or the running average)
+        auto put_x = [&](int t, double xn, bool was_nz, bool dense_x) {
+            if (kSparse) {
+                const bool nz = xn > 0.0;
+                st_flag(st.xflag + e0 + t, nz);
+                if (nz || was_nz || dense_x) st.x[e0 + t] = xn;
+                if (nz) red_add_f64(st.xsum + e0 + t, xn);
+            } else {
+                st.x[e0 + t] = xn;
+            }
+        };
 
         MQ_TA(13, 0, 1);  // tile visits
         for (;;) {
@@ -1441,11 +1722,13 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 MQ_TS(tq0);
                 MQ_TA(9, tc1, tq0);
                 double c[RP], u[RP];
+                uint32_t fb = 0;  // entries whose x^k was nonzero (sparse iterate)
 #pragma unroll
                 for (int e = 0; e < RP; ++e) {
                     const int t = a + lane + e * G;
                     if (t < b) {
-                        const double ue = su[t], xe = ldx(t);
+                        if (kSparse && sfl[t]) fb |= 1u << e;
+                        const double ue = su[t], xe = NGW > 0 ? 0.0 : ldxs(t);
                         double ce;
                         if (NGW > 0) {
                             ce = sc[t];
@@ -1475,9 +1758,9 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 if (has && lane == 0) st.srow[r0 + r] = sr;
                 const double inv_s = 1.0 / sr;
                 MQ_TS(tq2);
-                constexpr int XP = kXBDirect ? RP : 1;  // direct xbar: all loads in flight first
+                constexpr int XP = (kXBDirect && !kSparse) ? RP : 1;  // direct xbar: loads first
                 double xb[XP];
-                if (kXBDirect) {
+                if (kXBDirect && !kSparse) {
 #pragma unroll
                     for (int e = 0; e < XP; ++e) {
                         const int t = a + lane + e * G;
@@ -1493,8 +1776,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
 #else
                         const double xn = fmax(c[e] + tw * u[e] * inv_s, 0.0);
 #endif
-                        st.x[e0 + t] = xn;
-                        __stcs(st.xbar + e0 + t, av.wold * (kXBDirect ? xb[e % XP] : ldxb(t)) + av.wnew * xn);
+                        put_x(t, xn, (fb >> e) & 1u, false);
+                        if (!kSparse)
+                            __stcs(st.xbar + e0 + t,
+                                   av.wold * (kXBDirect ? xb[e % XP] : ldxb(t)) + av.wnew * xn);
                         if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
                     if (kBucket) st_keep(bslot + stp[t], xn, pkeep);
                     if (kAtomic && xn > 0.0) fixed_colsum_add(mk, st, scol[t], xn);
@@ -1508,7 +1793,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 // ---- longer rows: stream the row from shared memory
                 double s0p = 0.0, ap = 0.0, bp = 0.0;
                 for (int t = a + lane; t < b; t += G) {
-                    const double ue = su[t], xe = ldx(t);
+                    const double ue = su[t], xe = NGW > 0 ? 0.0 : ldxs(t);
                     double ce;
                     if (NGW > 0) {
                         ce = sc[t];
@@ -1531,8 +1816,9 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 const double inv_s = 1.0 / sr;
                 for (int t = a + lane; t < b; t += G) {
                     const double xn = fmax(sc[t] + tw * su[t] * inv_s, 0.0);
-                    st.x[e0 + t] = xn;
-                    __stcs(st.xbar + e0 + t, av.wold * ldxb(t) + av.wnew * xn);
+                    // x held c during the sweeps (direct mode): rewrite every entry
+                    put_x(t, xn, true, kXDirect);
+                    if (!kSparse) __stcs(st.xbar + e0 + t, av.wold * ldxb(t) + av.wnew * xn);
                     if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
                     if (kBucket) st_keep(bslot + stp[t], xn, pkeep);
                     if (kAtomic && xn > 0.0) fixed_colsum_add(mk, st, scol[t], xn);
@@ -1551,9 +1837,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         if (wl == 0) {
             // the last solver warp out of the tile publishes it (one gpu-scope
             // fence per tile, off the producer's path)
-            int prior;
-            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
-                         : "=r"(prior) : "r"(smem_addr(&claim[NSTAGE + s])) : "memory");
+            int prior = 0;
+            if (!kAtomic)  // only the block publication below needs the count
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                             : "=r"(prior) : "r"(smem_addr(&claim[NSTAGE + s])) : "memory");
 #ifndef MQ_NO_PUBLISH
             if (!kSplit && !kScatter && !kPhased && !kAtomic && prior == NSW - 1) {
                 __threadfence();
@@ -1685,7 +1972,12 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
             if (x_prev_out) x_prev_out[t] = xe;
             const double xn = fmax(xe - tau * st.p[mk.col[t]] + tw * mk.u[t] * inv_s, 0.0);
             st.x[t] = xn;
-            st.xbar[t] = av.wold * st.xbar[t] + av.wnew * xn;
+            if (kSparse) {
+                st.xflag[t] = xn > 0.0;
+                if (xn > 0.0) st.xsum[t] += xn;
+            } else {
+                st.xbar[t] = av.wold * st.xbar[t] + av.wnew * xn;
+            }
             if (kScatter) st.xc[mk.tpos[t]] = xn;
             if (kAtomic && xn > 0.0) fixed_colsum_add(mk, st, mk.col[t], xn);
         }
@@ -1805,6 +2097,16 @@ __global__ void colsum_finalize_kernel(int64_t m, const double *__restrict__ cs,
 
 __global__ void chunk_end_kernel(int64_t *navg, int iters) { *navg += iters; }
 
+// xbar = S / count (sparse iterate): the running average of kernels.py:138-142
+// from the running sum, once per chunk
+__global__ void avg_materialize_kernel(int64_t nnz, const double *__restrict__ xsum,
+                                       double *__restrict__ xbar, const int64_t *__restrict__ navg) {
+    const double count = (double)*navg;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x)
+        xbar[e] = count > 0.0 ? xsum[e] / count : xbar[e];
+}
+
 // ------------------------------------------------------------ launchers
 static int sm_count() {
     static int n = 0;
@@ -1824,7 +2126,7 @@ constexpr int kQMax = (kWCols + 31) / 32;  // goods per column-sum lane
 #else
 constexpr int kQMax = kNCW > 0 ? (1152 + kNCW * 32 - 1) / (kNCW * 32) : 1;  // goods per thread
 #endif
-using PrimalLayout = TileLayout<kEtile, MQ_TILE_ROWS, false>;
+using PrimalLayout = TileLayout<kEtile, MQ_TILE_ROWS, (kNGW > 0 && kXDirect)>;
 
 constexpr int kPrimalSmem = MQ_SMEM_PAD + kStages * PrimalLayout::kStage + 7 * kStages * 8 + 4 * kStages * 4 + 128 +
                             (kPhased ? kPhChunk * 8 : (kScatter || kSplit) ? 0 :
@@ -1968,7 +2270,8 @@ int mq_fast_chunk(const mq_market *mk, const mq_state *st, int iters, void *stre
         if ((rc = primal_launch(mk, st, it, nullptr, s))) return rc;
         if ((rc = colsum_rest_launch(mk, st, it, 1, s))) return rc;
     }
-    return mq_chunk_end(st, iters, stream);
+    if ((rc = mq_chunk_end(st, iters, stream))) return rc;
+    return mq_avg_materialize(mk, st, stream);
 }
 
 // debug: read and reset the wait-cycle counters (zeros unless built with
@@ -1988,6 +2291,15 @@ int mq_colsum_mode(void) {
 }
 
 int mq_bucket_slots(void) { return kBucket ? (int)kLag : 0; }
+int mq_x_sparse(void) { return kSparse ? 1 : 0; }
+
+int mq_avg_materialize(const mq_market *mk, const mq_state *st, void *stream) {
+    if (!kSparse) return 0;
+    if (!mk || !st) return set_error(cudaErrorInvalidValue, "mq_avg_materialize: null argument");
+    avg_materialize_kernel<<<grid_for(mk->nnz, 256, sm_count() * 16), 256, 0, (cudaStream_t)stream>>>(
+        mk->nnz, st->xsum, st->xbar, st->navg);
+    return check_launch("mq_avg_materialize");
+}
 int mq_fixed_colsum(void) { return kAtomic ? 1 : 0; }
 
 int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream) {

@@ -140,6 +140,9 @@ class NativeOps:
 
     def chunk_end(self, iters):
         self._c(self.lib.mq_chunk_end(self.eng.state, iters, _cur_stream()), "mq_chunk_end")
+        if self.eng.sparse:
+            self._c(self.lib.mq_avg_materialize(self.dm.struct, self.eng.state, _cur_stream()),
+                    "mq_avg_materialize")
 
     def resid_rows(self, x, p, use_norm, colbest, t_out, out, scratch):
         self._c(self.lib.mq_resid_rows(self.dm.struct, nat.ptr(x), nat.ptr(p), int(use_norm),
@@ -202,6 +205,13 @@ class PdhcgEngine:
         self.x = self._x_buf[:nnz]
         self.xbar = self._xbar_buf[:nnz]
         self.x0 = torch.zeros(nnz, **f64)
+        # sparse iterate: x > 0 flags and the running sum of x
+        self.sparse = bool(hasattr(dm, "lib") and dm.lib.mq_x_sparse() == 1
+                           and self.mode != "ksection")
+        self._xflag_buf = torch.ones(nnz + nat.PAD if self.sparse else 16, dtype=torch.uint8,
+                                     device=dev)
+        self.xflag = self._xflag_buf
+        self.xsum = torch.zeros(nnz if self.sparse else 1, **f64)
         # per-buyer utility of the last prox: the fused row solve's warm start
         self._srow_buf = torch.zeros(dm.n + nat.PAD, **f64)
         self.srow = self._srow_buf[:dm.n]
@@ -247,7 +257,7 @@ class PdhcgEngine:
             return None
         s = nat.MqState()
         for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "blk_done", "xc",
-                     "steps", "faults", "srow", "bucket"):
+                     "steps", "faults", "srow", "bucket", "xflag", "xsum"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.navg = self.navg_dev.data_ptr()
         s.pass_out = self.pass_buf.data_ptr()
@@ -267,6 +277,16 @@ class PdhcgEngine:
         return self._allreduce(out)
 
     # ------------------------------------------------------------ state
+    def _sparse_sync(self):
+        """After the host wrote x, xbar or navg: every x may be nonzero, and
+        the running sum restarts from navg * xbar."""
+        if self.sparse:
+            self.xflag.fill_(1)
+            if self.navg:
+                torch.mul(self.xbar, float(self.navg), out=self.xsum)
+            else:
+                self.xsum.zero_()
+
     def load_state(self, x, p):
         """Start (or warm start) from allocation x and prices p."""
         self.x.copy_(torch.as_tensor(x, dtype=torch.float64))
@@ -281,6 +301,7 @@ class PdhcgEngine:
         self.csbar.copy_(self.cs)
         self.navg = 0
         self.navg_dev.zero_()
+        self._sparse_sync()
         self.snapshot()
 
     def load_full_state(self, x, x_prev, p, xbar, pbar, navg):
@@ -301,6 +322,7 @@ class PdhcgEngine:
             self.colsum(xp, self.cs_prev)
         self.navg = int(navg)
         self.navg_dev.fill_(self.navg)
+        self._sparse_sync()
         self.snapshot()
 
     def initial_state(self, w_sum=None):
@@ -336,11 +358,14 @@ class PdhcgEngine:
             self.x_prev.copy_(self.x)
         self.navg = 0
         self.navg_dev.zero_()
+        self._sparse_sync()
 
     def adopt_average(self):
         self.x.copy_(self.xbar)
         self.p.copy_(self.pbar)
         self.cs.copy_(self.csbar)
+        if self.sparse:
+            self.xflag.fill_(1)
 
     # ------------------------------------------------------------ chunks
     def run_chunk(self, iters):

@@ -24,7 +24,7 @@ def test_native_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(lib, name)
-    assert lib.mq_abi_version() == 3
+    assert lib.mq_abi_version() == 4
     assert lib.mq_scratch_doubles() > 0
 
 
@@ -176,6 +176,8 @@ def test_abi_marshaling_without_device():
         "mq_colsum_mode": (),
         "mq_bucket_slots": (),
         "mq_fixed_colsum": (),
+        "mq_x_sparse": (),
+        "mq_avg_materialize": (mk, st, None),
         "mq_gen_fill": (0, 1, 10, 0, 0.5, 2.0, 1.0, 1, None, None, None, None, None),
         "mq_pdhcg_chunk": (0, 0, None, None, None, None, None, None, None, None, None, None,
                            None, 0, 0.1, 0.1, 32, 1e-10, 1, None, None, ctypes.byref(n64), None),
@@ -185,7 +187,7 @@ def test_abi_marshaling_without_device():
         if name == "mq_colsum_mode":
             assert rc in (0, 1, 2, 3, 4, 5)
             continue
-        if name in ("mq_bucket_slots", "mq_fixed_colsum"):
+        if name in ("mq_bucket_slots", "mq_fixed_colsum", "mq_x_sparse"):
             assert rc >= 0
             continue
         assert rc != 0, name
