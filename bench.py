@@ -200,14 +200,21 @@ def kernel_breakdown(eng, iters):
             eng._allreduce(eng.cs)
             nat.check(lib.mq_colsum_finalize(mk, st, it, s), "finalize")
         e[3].record()
-    nat.check(lib.mq_chunk_end(st, iters, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
-              "chunk_end")
+    cur = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nat.check(lib.mq_chunk_end(st, iters, cur), "chunk_end")
+    if eng.sparse:
+        nat.check(lib.mq_avg_materialize(mk, st, cur), "avg_materialize")
     torch.cuda.synchronize()
     eng.navg += iters
     t = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])]
                   for e in ev])
     passes = int(eng.pass_buf[:iters].sum().item())
     return t.mean(axis=0), passes
+
+
+# random 8-byte gathers from an L2-resident 800 KB vector, 148 SMs, 164 KB of
+# shared memory per SM (the fused kernel's carveout): profiles/micro_gather_l1.txt
+GATHER_PEAK = 2.66e11
 
 
 def traffic_from_profile(name):
@@ -327,18 +334,25 @@ def main():
         dist.barrier()
     value = a.steps / (t_ms / 1e3)
     # kernels launched in the timed region: dual + non-empty primal bins + colsum
-    # per iteration, chunk_end per chunk (+ finalize on N>1)
+    # per iteration, chunk_end (+ the running-average materialization) per chunk
+    # (+ finalize on N>1)
     primal_kernels = int(dm.tiles.shape[0] > 0) + int(dm.long_rows.numel() > 0)
     per_it = 2 + primal_kernels + (1 if world > 1 else 0)
-    launches = a.steps * per_it + -(-a.steps // 40)
+    launches = a.steps * per_it + -(-a.steps // 40) * (1 + int(eng.sparse))
 
     # per-kernel breakdown and the primal kernel's roofline
     kt, kpass = kernel_breakdown(eng, a.breakdown_iters)
     n_local = dm.n
-    # fused kernel = prox + averages (44 B/nnz + 20 B/row + p) and the column
-    # sums of the new x (bperm 4 + x 8 B/nnz): DESIGN.md §5.1
+    # algorithmic bytes of one iteration's nnz sweep in the dense formulation
+    # (prox + averages 44 B/nnz, column sums 12 B/nnz, + rows and
+    # goods).  The default kernel skips the ~99 % zero entries of x (sparse
+    # iterate), so its DRAM traffic is far lower (`dram_*`);
+    # its binding resource is the random L2 gather of p[col], one 32-byte
+    # sector per entry (`gather_*`, peak = tools/micro/gather_l1.cu)
     primal_bytes = 56 * nnz_local + 20 * n_local + 8 * m
     achieved = primal_bytes / (kt[1] / 1e3) / 1e9
+    traffic = traffic_from_profile("primal")
+    gathers_per_s = nnz_local / (kt[1] / 1e3)
     iter_bytes = 56 * nnz_full + 16 * n_full + 48 * m      # SURVEY §8(d) B_iter
     iter_gbs = iter_bytes / (t_ms / 1e3 / a.steps) / 1e9 / world
 
@@ -356,8 +370,19 @@ def main():
                      "kernel": "primal_fused_kernel (exact prox + averages + column sums)",
                      "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4),
-                     "traffic": traffic_from_profile("primal"), "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": primal_bytes},
+                     "traffic": traffic, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": primal_bytes,
+                     "note": "achieved = SURVEY 8(d) algorithmic bytes (dense formulation) / "
+                             "kernel time; the sparse-iterate kernel does not move the zero "
+                             "entries of x, see dram_* for its own traffic and gather_* for "
+                             "the resource that binds it",
+                     "dram_achieved": (round(traffic / (kt[1] / 1e3) / 1e9, 1)
+                                       if traffic else None),
+                     "dram_frac": (round(traffic / (kt[1] / 1e3) / 1e9 / hbm_peak, 4)
+                                   if traffic else None),
+                     "gather_achieved": round(gathers_per_s / 1e9, 1),
+                     "gather_peak": GATHER_PEAK / 1e9, "gather_unit": "G random 8-byte L2 "
+                     "gathers/s", "gather_frac": round(gathers_per_s / GATHER_PEAK, 4)},
         "iteration_roofline": {"bytes_per_iteration": iter_bytes,
                                "achieved_gbs_per_gpu": round(iter_gbs, 1),
                                "frac": round(iter_gbs / hbm_peak, 4)},
