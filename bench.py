@@ -217,12 +217,14 @@ def kernel_breakdown(eng, iters):
 GATHER_PEAK = 2.66e11
 
 
-def traffic_from_profile(name):
+def traffic_from_profile(name, config):
+    """ncu DRAM bytes per launch of `name` on `config` (profiles/ncu_traffic.json,
+    written by tools/ncu_summary.py from the round's full capture), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
-            d = json.load(fh)
-        return d.get(name, {}).get("dram_bytes_per_launch")
+            d = json.load(fh).get(name, {})
+        return d.get("dram_bytes_per_launch") if d.get("config", "c4") == config else None
     except Exception:
         return None
 
@@ -351,7 +353,7 @@ def main():
     # sector per entry (`gather_*`, peak = tools/micro/gather_l1.cu)
     primal_bytes = 56 * nnz_local + 20 * n_local + 8 * m
     achieved = primal_bytes / (kt[1] / 1e3) / 1e9
-    traffic = traffic_from_profile("primal")
+    traffic = traffic_from_profile("primal", a.config)
     gathers_per_s = nnz_local / (kt[1] / 1e3)
     iter_bytes = 56 * nnz_full + 16 * n_full + 48 * m      # SURVEY §8(d) B_iter
     iter_gbs = iter_bytes / (t_ms / 1e3 / a.steps) / 1e9 / world

@@ -53,7 +53,8 @@ for name, d in out.items():
         rd = gb(*d["dram__bytes_read.sum"])
         wr = gb(*d["dram__bytes_write.sum"])
         traffic["primal"] = {"dram_bytes_per_launch": (rd + wr) * 1e9, "read_gb": rd,
-                             "write_gb": wr, "kernel": name, "source": rep}
+                             "write_gb": wr, "kernel": name, "source": rep,
+                             "config": "c4"}  # tools/measure_round.sh profiles config 4
 json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
 # launch list: per-kernel share of device time
 tot = defaultdict(float)
