@@ -223,7 +223,9 @@ class PdhcgEngine:
         slots = int(dm.lib.mq_bucket_slots()) if hasattr(dm, "lib") else 0
         nb = slots * int(getattr(dm, "bcap", 0))
         fixed = getattr(getattr(dm, "lib", None), "mq_fixed_colsum", None)
-        if fixed is not None and fixed() == 1:  # experiment build: fixed-point column sums
+        # fixed-point column sums (default build): m u64 accumulators
+        self.fixed = bool(fixed is not None and fixed() == 1 and self.mode != "ksection")
+        if self.fixed:
             nb = max(nb, m)
         self.bucket = torch.zeros(max(1, nb), **f64)
         self.p = torch.zeros(m, **f64)
@@ -249,6 +251,15 @@ class PdhcgEngine:
         self.navg = 0
         self.tau = self.sigma = None
         self._graphs = {}
+        if self.fixed and self.world > 1:
+            # one fixed-point scale on every rank (from the global column
+            # counts), so the ranks' integer column sums add exactly: the
+            # all-reduce runs on the u64 accumulators and the N-rank column
+            # sums are bitwise the 1-rank ones
+            from .device import fixed_point_scale
+
+            gmax = int(self._global_counts().max().item()) if m else 1
+            dm.struct.cs_scale, dm.struct.cs_xmax = fixed_point_scale(gmax)
         self.state = self._make_state()
 
     # ------------------------------------------------------------ plumbing
@@ -396,9 +407,14 @@ class PdhcgEngine:
         self.pass_buf[:iters].zero_()
         self.faults.zero_()
         single = self.world == 1
+        exact = self.fixed and not single
         for it in range(iters):
             ops.dual(it)
             ops.primal(it)
+            if exact:  # integer all-reduce of the fixed-point sums, then convert
+                self._allreduce(self.bucket.view(torch.int64)[:self.dm.m])
+                ops.colsum_rest(it, True)
+                continue
             ops.colsum_rest(it, single)
             if not single:
                 self._allreduce(self.cs)

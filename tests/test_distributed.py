@@ -98,3 +98,57 @@ def test_shard_bounds_balance_entries():
     sizes = [rp[h] - rp[l] for l, h in b]
     assert b[0][0] == 0 and b[-1][1] == 1000
     assert max(sizes) - min(sizes) <= 2 * 50 * 3
+
+
+# ---------------------------------------------------------------- GPU ranks
+def _gpu_worker(rank, world, port, name, out_dir):
+    """One rank of the sharded device path: its rows' DeviceMarket on cuda:0,
+    the engine's per-iteration all-reduce of the fixed-point column sums and
+    the check-time reductions over gloo (the kernels of the two ranks never
+    wait on each other; only the host-driven collectives couple them)."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(__file__))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(__file__)))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_06258_b200.device import DeviceMarket
+    from paper_2506_06258_b200.driver import DeviceSession, solve_on_device
+
+    g = golden(name)
+    inst = instance_from(g)
+    u = inst.utilities
+    lo, hi = shard_bounds(u.row_offsets, world)[rank]
+    rp = u.row_offsets[lo:hi + 1] - u.row_offsets[lo]
+    e0, e1 = int(u.row_offsets[lo]), int(u.row_offsets[hi])
+    dm = DeviceMarket(rp, u.col_indices[e0:e1], u.values[e0:e1], inst.budgets[lo:hi],
+                      u.n_cols, row_begin=lo)
+    cfg = _cfg(g)
+    sess = DeviceSession(None, cfg, group=dist.group.WORLD, dm=dm)
+    rep = solve_on_device(sess, cfg, w_sum=float(np.sum(inst.budgets)))
+    np.savez(os.path.join(out_dir, f"grank{rank}.npz"), prices=rep.prices,
+             allocation=rep.allocation, iters=rep.inner_iterations, restarts=rep.restarts,
+             lo=lo, hi=hi)
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["solve_medium.npz", "solve_g200_tol0.npz"])
+def test_two_rank_device_solve_matches_single_rank(name, tmp_path):
+    import paper_2506_06258_b200 as mq
+
+    g = golden(name)
+    inst = instance_from(g)
+    one = mq.run_solve(inst, _cfg(g), "pdhcg")
+    mp.start_processes(_gpu_worker, args=(2, _free_port(), name, str(tmp_path)), nprocs=2,
+                       start_method="spawn")
+    r = [np.load(tmp_path / f"grank{k}.npz") for k in range(2)]
+    for k in range(2):
+        assert int(r[k]["iters"]) == one.inner_iterations == int(g["iters"])
+        assert int(r[k]["restarts"]) == one.restarts == int(g["restarts"])
+        assert rel_max(r[k]["prices"], one.prices) <= 1e-9
+    alloc = np.concatenate([r[0]["allocation"], r[1]["allocation"]])
+    assert np.allclose(alloc, one.allocation, rtol=1e-8, atol=1e-12)

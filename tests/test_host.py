@@ -270,3 +270,20 @@ def test_blocked_schedule_preserves_column_order():
             seg = bperm[bptr[b * m + j]:bptr[b * m + j + 1]]
             blk = np.searchsorted(tstart[::6], seg, side="right") - 1
             assert np.all(blk == b)
+
+
+def test_fixed_point_scale_cannot_overflow():
+    """The fixed-point column sums: cs_xmax * cs_scale * (entries of the
+    fullest good) <= 2^62, so no u64 accumulator can overflow; the scale is a
+    power of two between 2^24 and 2^48 (resolution <= 6e-8)."""
+    import math
+
+    from paper_2506_06258_b200.device import fixed_point_scale
+
+    for c in [0, 1, 7, 500, 1000, 10_000, 123_457, 10**6, 10**8, 2**31]:
+        scale, xmax = fixed_point_scale(c)
+        k = math.log2(scale)
+        assert k == int(k) and 24 <= k <= 48
+        assert xmax * scale * max(1, c) <= 2.0 ** 62 * (1 + 1e-12)
+        if c <= 10**6:
+            assert xmax >= 1024
