@@ -43,10 +43,12 @@
 #endif
 #endif
 #ifndef MQ_NSW
-#ifdef MQ_CS_DENSE
+#if defined(MQ_CS_DENSE)
 #define MQ_NSW 15
-#else
+#elif defined(MQ_X_DENSE) || defined(MQ_NO_XPREFETCH)
 #define MQ_NSW 19  /* no column-sum warps: 20 warps at 96 registers */
+#else
+#define MQ_NSW 18  /* + the x-prefetch warp: 20 warps at 96 registers */
 #endif
 #endif
 #ifndef MQ_NGW
@@ -435,12 +437,12 @@ __device__ __forceinline__ double row_root_warm(const double (&c)[PER], UF u,
                     done = true;  // no entry with u > 0
                 }
             } else {
-                const double g0 = A0 + tw * B0 / s0;
-                if (g0 >= s0) {
+                // g(s0) = A0 + tw B0 / s0 >= s0, without the division
+                if (fma(A0, s0, tw * B0) >= s0 * s0) {
                     s = fmax(active_root(A0, B0, tw), s0);
                     prev = msk;
                 } else {
-                    s = g0;  // lower bound; its active set is still unknown
+                    s = A0 + tw * B0 / s0;  // g(s0): a lower bound, active set unknown
                     force = true;
                 }
             }
@@ -529,6 +531,14 @@ constexpr bool kXBDirect = true;  // xbar likewise
 constexpr bool kXBDirect = kSparse;
 #endif
 static_assert(!kSparse || kAtomic, "the sparse iterate needs the fixed-point column sums");
+// one extra warp that, a tile or two ahead of the solvers, pulls the flagged
+// (nonzero) x of each staged tile into L2 (otherwise scattered DRAM reads on
+// the solvers' critical path)
+#if !defined(MQ_NO_XPREFETCH)
+constexpr int kPF = kSparse ? 1 : 0;  // (the default MQ_NSW drops to 18 to keep 20 warps)
+#else
+constexpr int kPF = 0;
+#endif
 static_assert(!(kXDirect || kXBDirect) || ((MQ_NGW == 0 || kSparse) && !kPhased && !kScatter && !kSplit),
               "direct x/xbar loads: default (fused) mode only");        // gathered values staged per round (phased mode)
 
@@ -738,7 +748,7 @@ __device__ __forceinline__ void phased_gather(const mq_market &mk, const mq_stat
 // from a shared counter, so no solver waits for another inside a tile, and
 // they never touch global memory before their stores.
 template <int G, int NSW, int NGW, int NCW, int ETILE, int RTILE, int NSTAGE, int QMAX>
-__global__ void __launch_bounds__((NSW + NGW + NCW + 1) * 32, 1)
+__global__ void __launch_bounds__((NSW + NGW + NCW + 1 + kPF) * 32, 1)
 primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
                     int write_cs, int64_t tile_lo, int64_t tile_hi, int *tile_ctr) {
     // c (gather warps) is written over the staged x, or into its own region
@@ -766,6 +776,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             mbar_init(&empty[s], NSW);
             mbar_init(&ready[s], NGW > 0 ? NGW : 1);
         }
+        claim[2 * NSTAGE] = 0;  // producer done (read by the x-prefetch warp)
         mbar_fence_init();
     }
     __syncthreads();
@@ -881,6 +892,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 if (k >= tile_hi) {  // sentinel: consumers leave
                     stile[s] = -1;
                     mbar_expect_tx(&full[s], 0);
+                    *reinterpret_cast<volatile int *>(&claim[2 * NSTAGE]) = 1;
                     break;
                 }
                 const int64_t r0 = m01.x, r1 = m01.y, e0 = m23.x, cnt = m23.y - m23.x;
@@ -1005,6 +1017,46 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             for (int q = 0; q < PQ; ++q) {
                 const int jl = pt + q * NP;
                 if (jl < ph_nc) st.cs[ph_lo + jl] = ph_acc[q];
+            }
+        }
+        return;
+    }
+    if (kPF && warp == NSW + NGW + NCW + 1) {  // ------------- x prefetch (sparse)
+        // Follows the full barriers only (never holds a stage): for each
+        // staged tile, the flagged entries' x go to L2 with prefetch hints.
+        // A late look at a refilled stage only prefetches other valid x.
+        for (int64_t j = 0;; ++j) {
+            const int s = (int)(j % NSTAGE);
+            const uint32_t par = (uint32_t)((j / NSTAGE) & 1);
+            bool ok = false;
+            for (;;) {  // bounded: stop once the producer has posted the sentinel
+                ok = __shfl_sync(MQ_FULL, (int)mbar_test(&full[s], par), 0) != 0;
+                if (ok || *reinterpret_cast<volatile int *>(&claim[2 * NSTAGE])) break;
+                __nanosleep(64);
+            }
+            if (!ok) break;
+            const int64_t k = stile[s];
+            if (k < 0) break;
+            // the tile's extent from global memory (consistent even if this
+            // warp is late and the stage already holds a newer tile)
+            const int64_t e0 = __ldg(mk.tiles + 4 * k + 2);
+            const int64_t cnt = __ldg(mk.tiles + 4 * k + 3) - e0;
+            const unsigned char *fl = smem + s * L::kStage + L::kF;
+            const int lead = (int)(e0 & 15);
+            int nw = (lead + (int)cnt + 15) >> 4;
+            nw = nw < (ETILE + 32) / 16 ? nw : (ETILE + 32) / 16;
+            for (int w16 = wl; w16 < nw; w16 += 32) {
+                const uint4 v = reinterpret_cast<const uint4 *>(fl)[w16];
+                const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                    for (int by = 0; by < 4; ++by) {
+                        const int t = w16 * 16 + q * 4 + by - lead;
+                        if (((wd[q] >> (8 * by)) & 0xffu) && t >= 0 && t < cnt && e0 + t < mk.nnz)
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(st.x + e0 + t));
+                    }
+                }
             }
         }
         return;
@@ -2149,7 +2201,7 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
         if (e != cudaSuccess) return set_error(e, "mq_primal_step: smem attribute");
         configured = true;
     }
-    const int nthr = (kNSW + kNGW + kNCW + 1) * 32;
+    const int nthr = (kNSW + kNGW + kNCW + 1 + kPF) * 32;
     if (mk->ntiles > 0 && kSplit) {
         // per block of tiles: the primal sweep, then the block's column sums
         // while its x is still in L2
