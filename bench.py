@@ -297,10 +297,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the N-rank path on a 1-GPU box: every rank on cuda:0,
+    # gloo collectives (numbers meaningless; never used for measurements)
+    shared = os.environ.get("MQ_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
     if a.impl == "reference":
         return reference_arm(a, rank, world)

@@ -1734,11 +1734,18 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         };
 
         MQ_TA(13, 0, 1);  // tile visits
+#ifdef MQ_STATIC_PAIRS
+        // static: warp w takes row pairs w, w + NSW, ... of the tile (no claims)
+        for (int pp = warp;; pp += NSW) {
+            MQ_TS(tc0);
+            const int rb = pp * GPW;
+#else
         for (;;) {
             MQ_TS(tc0);
             int rb = 0;
             if (wl == 0) rb = atomicAdd(&claim[s], GPW);
             rb = __shfl_sync(MQ_FULL, rb, 0);
+#endif
             MQ_TS(tc1);
             MQ_TA(8, tc0, tc1);
             if (rb >= nrows) break;  // warp-uniform
