@@ -12,6 +12,7 @@ Fixtures (all float64 stored exactly):
   chunk_*.npz    state -> kernels.pdhcg_chunk(iters) -> state   (kernel vectors)
   rowroot.npz    rows  -> kernels._row_root                      (row-solver vectors)
   solve_*.npz    instance -> run_solve(...) report               (full solves)
+  pdhg_*.npz     instance -> run_solve(..., "pdhg") report       (lifted PDHG solves)
   resid.npz      random states -> kkt.residuals_compact           (residual formulas)
   exchange.npz   generate_exchange -> solve_exchange trace       (Arrow-Debreu)
   gen.json       generator fingerprints (instance_fingerprint)   (generator parity)
@@ -178,7 +179,7 @@ def report_arrays(rep, with_alloc=True):
     d = dict(status=rep.status, iters=rep.inner_iterations, restarts=rep.restarts,
              prices=rep.prices, utility_values=rep.utility_values,
              dual_values=rep.dual_values,
-             passes=np.asarray(rep.subproblem_passes, dtype=np.int64),
+             passes=np.asarray(rep.subproblem_passes or [], dtype=np.int64),
              history=np.asarray(rep.residual_history, dtype=np.float64),
              final=np.array([rep.final_residuals.r_primal, rep.final_residuals.r_dual,
                              rep.final_residuals.r_gap, rep.final_residuals.rel_kkt]),
@@ -215,6 +216,49 @@ def solve_case(name, inst, cfg, store_instance, with_alloc=True):
     print(f"  {name}: {rep.status} iters={rep.inner_iterations} restarts={rep.restarts} "
           f"obj={obj!r} ref {t_ref:.1f}s oracle {t_orc:.1f}s")
     return rep
+
+
+def pdhg_case(name, inst, cfg):
+    """Lifted PDHG (algo="pdhg", driver.py:184-268): the reference's report,
+    written only if oracle.solve_lifted reproduces it bit for bit."""
+    t = time.time()
+    rep = me.run_solve(inst, cfg, "pdhg")
+    t_ref = time.time() - t
+    o = orc.solve_lifted(to_mk(inst), tol=cfg.tol, max_iters=cfg.max_iters,
+                         check_every=cfg.check_every, restart=cfg.restart,
+                         restart_k=cfg.restart_k, step_mode=cfg.step_mode,
+                         adapt_eta=cfg.adapt_eta)
+    assert rep.inner_iterations == o["inner_iterations"] and rep.restarts == o["restarts"], name
+    assert same(rep.prices, o["prices"]) and same(rep.allocation, o["allocation"]), name
+    assert same(rep.utility_values, o["utility_values"]), name
+    assert same(rep.dual_values, o["dual_values"]), name
+    assert list(rep.residual_history) == o["residual_history"], name
+    obj = me.kkt.eg_objective(inst, rep.allocation)
+    assert obj == o["objective"], name
+    u = inst.utilities
+    d = report_arrays(rep, True)
+    d.pop("passes")
+    save(f"pdhg_{name}.npz", **d, objective=obj, tol=cfg.tol, restart=cfg.restart,
+         restart_k=cfg.restart_k, step_mode=cfg.step_mode, max_iters=cfg.max_iters,
+         ref_seconds=t_ref, n=u.n_rows, m=u.n_cols, indptr=u.row_offsets, col=u.col_indices,
+         u=u.values, w=inst.budgets)
+    print(f"  pdhg {name}: {rep.status} iters={rep.inner_iterations} restarts={rep.restarts} "
+          f"obj={obj!r} ref {t_ref:.1f}s")
+
+
+def pdhg_cases():
+    tiny = me.FisherInstance(me.SparseMatrix.from_dense([[.8, .3], [.2, .9], [.5, .5]]),
+                             np.array([.4, .7, .9]))
+    pdhg_case("tiny", tiny, me.SolveConfig(tol=1e-7, max_iters=100_000))
+    pdhg_case("small", me.generate_fisher(me.GeneratorConfig(n=12, m=6, sparsity_u=0.5, seed=3)),
+              me.SolveConfig(tol=1e-6))
+    pdhg_case("medium", me.generate_fisher(me.GeneratorConfig(n=60, m=25, sparsity_u=0.3, seed=11)),
+              me.SolveConfig(tol=1e-5))
+    g = me.generate_fisher(me.GeneratorConfig(n=200, m=80, sparsity_u=0.2, seed=1))
+    pdhg_case("g200", g, me.SolveConfig(tol=1e-4))
+    g = me.generate_fisher(me.GeneratorConfig(n=80, m=30, sparsity_u=0.3, seed=5))
+    pdhg_case("g80_fixed", g, me.SolveConfig(tol=1e-5, restart="fixed", restart_k=120))
+    pdhg_case("g80_theory", g, me.SolveConfig(tol=1e-3, step_mode="theory", max_iters=6000))
 
 
 def c1_instance():
@@ -367,6 +411,7 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     orc.set_threads(os.cpu_count())
     steps = {"chunk": chunk_cases, "rowroot": rowroot_cases, "solve": lambda: solve_cases(a.big),
+             "pdhg": pdhg_cases,
              "bigsolve": big_solve_cases,
              "resid": resid_cases, "exchange": exchange_case,
              "gen": lambda: gen_fingerprints(a.big), "c2": c2_lockstep}

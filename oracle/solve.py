@@ -411,6 +411,157 @@ def solve(mk, tol=1e-4, max_iters=100_000, sections=32, subtol=1e-10,
     }
 
 
+# ------------------------------------------------------------ lifted PDHG
+
+def pdhg_chunk(nm, x, x_prev, t, t_prev, p, y, xbar, tbar, pbar, ybar, navg, tau, sigma,
+               iters):
+    """kernels.py:146-197 (pdhg_chunk) in numpy, same operations in the same
+    order: the column sums accumulate each column in ascending row order and
+    the row sums each row in storage order (np.bincount is sequential), every
+    elementwise step rounds as numba's (no contraction).  In place; returns
+    the new navg."""
+    count = navg
+    for _ in range(iters):
+        ext = 2.0 * x - x_prev
+        p += sigma * (nm.col_sums(ext) - 1.0)
+        acc = nm.row_sums(nm.val * ext)
+        y += sigma * ((2.0 * t - t_prev) - acc)
+        x_prev[:] = x
+        t_prev[:] = t
+        d = tau * y - t_prev
+        root = np.sqrt(d * d + 4.0 * tau * nm.w)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            conj = 2.0 * tau * nm.w / (d + root)
+        t[:] = np.where(d > 0.0, conj, 0.5 * (root - d))
+        xv = x_prev - tau * (p[nm.col] - nm.val * y[nm.row_ids])
+        x[:] = np.where(xv > 0.0, xv, 0.0)
+        count += 1
+        wold = (count - 1.0) / count
+        wnew = 1.0 / count
+        xbar[:] = wold * xbar + wnew * x
+        tbar[:] = wold * tbar + wnew * t
+        ybar[:] = wold * ybar + wnew * y
+        pbar[:] = wold * pbar + wnew * p
+    return count
+
+
+def lifted_op_norm(nm, iters=50):
+    """pdhg.py:144-166: power iteration on (x, t) -> (colsum x, t - u.x)."""
+    nnz, n = nm.nnz, nm.n
+    v = np.full(nnz + n, 1.0 / np.sqrt(nnz + n))
+    sig = 0.0
+    for _ in range(iters):
+        vx, vt = v[:nnz], v[nnz:]
+        out_p = nm.col_sums(vx)
+        out_y = vt - nm.row_sums(nm.val * vx)
+        back_x = out_p[nm.col] - nm.val * out_y[nm.row_ids]
+        wv = np.concatenate([back_x, out_y])
+        sig = np.linalg.norm(wv)
+        if sig == 0.0:
+            return 0.0
+        v = wv / sig
+    return float(np.sqrt(sig))
+
+
+def solve_lifted(mk, tol=1e-4, max_iters=100_000, check_every=40, step_mode="adaptive",
+                 adapt_eta=True, restart="adaptive", restart_k=0, beta=(0.2, 0.8, 0.2)):
+    """Restarted lifted PDHG (driver.py:184-268 _LiftedRun inside the loop of
+    driver.py:271-377, algo="pdhg"); returns a dict with the SolveReport
+    fields (plus "objective")."""
+    bad = validate(mk)
+    if bad:
+        raise ValueError("; ".join(bad))
+    nm, scales = normalize(mk)
+    counts = np.bincount(nm.col, minlength=nm.m)
+    x = 1.0 / counts[nm.col].astype(np.float64)          # pdhg.py:60-68
+    t = nm.row_sums(nm.val * x)
+    p = np.full(nm.m, float(np.sum(nm.w)) / nm.m)
+    y = nm.w / t
+    x_prev, t_prev = x.copy(), t.copy()
+    xbar, tbar, pbar, ybar = x.copy(), t.copy(), p.copy(), y.copy()
+    navg = 0
+    L = max(lifted_op_norm(nm), np.finfo(float).tiny)
+
+    if step_mode == "theory":
+        steps = None
+        tau = sigma = 1.0 / (2.0 * L)
+    else:
+        primal = np.linalg.norm(np.concatenate([nm.col_sums(x) - 1.0,
+                                                t - nm.row_sums(nm.val * x)]))
+        uy = nm.val * y[nm.row_ids]
+        best = np.full(nm.m, -np.inf)
+        np.maximum.at(best, nm.col, uy)
+        dual = np.linalg.norm(np.concatenate([nm.w / t - y, np.minimum(p - best, 0.0)]))
+        primal, dual = float(primal), float(dual)
+        omega0 = max(1.0, dual / primal) if (primal > 1e-8 and dual > 1e-8) else 1.0
+        steps = Steps(0.9 / L, omega0, 0.95 / L, omega0 / OMEGA_BOUND_FACTOR,
+                      omega0 * OMEGA_BOUND_FACTOR)
+        tau, sigma = steps.tau, steps.sigma
+
+    def res(xx, tt, pp, yy):
+        return residuals_lifted(mk, xx, tt * scales, pp, yy / scales)
+
+    res_avg = res(xbar, tbar, pbar, ybar)
+    at_restart = prev_check = res_avg[3]
+    snap = (x.copy(), t.copy(), p.copy(), y.copy())
+    history = []
+    total = restarts = 0
+    t0 = time.perf_counter()
+    while True:
+        chunk = min(check_every, max_iters - total)
+        if restart == "fixed":
+            chunk = min(chunk, restart_k - navg)
+        navg = pdhg_chunk(nm, x, x_prev, t, t_prev, p, y, xbar, tbar, pbar, ybar, navg,
+                          tau, sigma, chunk)
+        total += chunk
+        res_last = res(x, t, p, y)
+        res_avg = res(xbar, tbar, pbar, ybar)
+        metric = min(res_last[3], res_avg[3])
+        history.append((total, metric))
+        if metric <= tol or total >= max_iters:
+            if res_avg[3] < res_last[3]:
+                x, t, p, y = xbar.copy(), tbar.copy(), pbar.copy(), ybar.copy()
+                final = res_avg
+            else:
+                final = res_last
+            status = "optimal" if metric <= tol else "max-iters"
+            break
+        if restart == "fixed":
+            do_restart = navg >= restart_k
+        else:
+            do_restart = should_restart(res_avg[3], at_restart, prev_check, navg, total, beta)
+        prev_check = res_avg[3]
+        if do_restart:
+            if steps is not None:
+                dx, dt = xbar - snap[0], tbar - snap[1]
+                dp, dy = pbar - snap[2], ybar - snap[3]
+                k_dx_p = float(np.dot(nm.col_sums(dx), dp))
+                k_dt_y = float(np.dot(dt - nm.row_sums(nm.val * dx), dy))
+                psq = float(np.dot(dx, dx) + np.dot(dt, dt))
+                dsq = float(np.dot(dp, dp) + np.dot(dy, dy))
+                inter = abs(k_dx_p + k_dt_y)
+                eta_obs = None
+                if adapt_eta and inter > 0.0:
+                    eta_obs = (steps.omega * psq + dsq / steps.omega) / (2.0 * inter)
+                steps.update(float(np.sqrt(psq)), float(np.sqrt(dsq)), eta_obs)
+                tau, sigma = steps.tau, steps.sigma
+            x[:], t[:], p[:], y[:] = xbar, tbar, pbar, ybar
+            x_prev[:] = x
+            t_prev[:] = t
+            navg = 0
+            restarts += 1
+            snap = (x.copy(), t.copy(), p.copy(), y.copy())
+            at_restart = prev_check = res_avg[3]
+    wall = time.perf_counter() - t0
+    return {
+        "status": status, "inner_iterations": total, "restarts": restarts,
+        "wall_time_seconds": wall, "final_residuals": final,
+        "residual_history": history, "prices": p.copy(), "allocation": x.copy(),
+        "utility_values": t * scales, "dual_values": y / scales,
+        "objective": eg_objective(mk, x), "op_norm": L, "tau_sigma": (tau, sigma),
+    }
+
+
 # ---------------------------------------------------------- Arrow-Debreu loop
 
 def apply_T(U, E, w, tol=1e-6, warm_start=None, **kw):

@@ -88,6 +88,24 @@ def test_oracle_solve_bit_exact(name, oracle):
     assert o["objective"] == float(g["objective"])
 
 
+@pytest.mark.parametrize("name", golden_names("pdhg_"))
+def test_oracle_lifted_pdhg_bit_exact(name, oracle):
+    """Lifted PDHG (kernels.py:146-197, driver.py:184-268): the oracle's
+    restatement reproduces the reference's solve bit for bit."""
+    g = golden(name)
+    inst = instance_from(g)
+    o = oracle.solve_lifted(oracle_market(inst), tol=float(g["tol"]),
+                            max_iters=int(g["max_iters"]), restart=str(g["restart"]),
+                            restart_k=int(g["restart_k"]), step_mode=str(g["step_mode"]))
+    assert o["status"] == str(g["status"])
+    assert o["inner_iterations"] == int(g["iters"]) and o["restarts"] == int(g["restarts"])
+    for k in ("prices", "allocation", "utility_values", "dual_values"):
+        assert np.array_equal(o[k], g[k]), k
+    assert np.array_equal(np.asarray(o["residual_history"]), g["history"])
+    assert np.array_equal(np.asarray(o["final_residuals"]), g["final"])
+    assert o["objective"] == float(g["objective"])
+
+
 @pytest.mark.slow
 def test_oracle_solve_spec1000(oracle):
     import paper_2506_06258_b200 as mq
