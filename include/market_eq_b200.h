@@ -122,6 +122,22 @@ typedef struct mq_state {
     double *xsum;     /* [nnz]                                                */
 } mq_state;
 
+/* Mutable iterate of the lifted PDHG path (algo="pdhg", kernels.py:146-197):
+ * x (nnz), t and y (n), p (m), their running averages, and the row sums
+ * ru = u.x^k, ru_prev = u.x^{k-1} (normalized utilities) that stand in for the
+ * reference's x_prev in the y step. */
+typedef struct mq_lstate {
+    double *x, *xbar;                        /* [nnz]                          */
+    double *t, *t_prev, *tbar, *y, *ybar;    /* [n]                            */
+    double *ru, *ru_prev;                    /* [n]                            */
+    double *p, *pbar, *cs, *cs_prev, *csbar; /* [m]                            */
+    unsigned long long *fix;                 /* [m] fixed-point column sums,
+                                                zero between iterations        */
+    const double *steps;                     /* [2] tau, sigma                 */
+    int64_t *navg;                           /* [1]                            */
+    int64_t *faults;                         /* [1] x beyond cs_xmax           */
+} mq_lstate;
+
 /* ---- faithful drop-in ------------------------------------------------------
  * Replaces kernels.pdhcg_chunk (kernels.py:99-145) argument for argument:
  * same in-place semantics for x, x_prev, p, xbar, pbar, c_buf and
@@ -198,6 +214,38 @@ int mq_resid_cols(int64_t m, const double *cs, const double *p, const double *co
 int mq_restart_moves(const mq_market *mk, const double *xbar, const double *x0,
                      const double *pbar, const double *p0, const double *csbar,
                      const double *cs0, double *out, double *scratch, void *stream);
+
+/* ---- lifted PDHG (algo="pdhg") ------------------------------------------
+ * One iteration (kernels.py:158-196): price step, per-buyer y/t update and the
+ * entry-wise x update with the averages, fixed-point column sums of x. */
+int mq_pdhg_step(const mq_market *mk, const mq_lstate *ls, int it, void *stream);
+/* N ranks: mq_pdhg_step without the column-sum conversion; the host
+ * all-reduces ls->fix (int64) and then calls mq_pdhg_finish_colsum. */
+int mq_pdhg_colsum_only(const mq_market *mk, const mq_lstate *ls, int it, void *stream);
+int mq_pdhg_finish_colsum(const mq_market *mk, const mq_lstate *ls, int it, void *stream);
+int mq_pdhg_chunk_end(const mq_lstate *ls, int iters, void *stream);
+/* out_i = u_i . x_i (use_norm: normalized utilities, else original). */
+int mq_row_dot(const mq_market *mk, const double *x, int use_norm, double *out, void *stream);
+/* residuals_lifted (kkt.py:29-76) row/entry part for (x, t*s, p, y/s), s =
+ * scales (use_norm = 0) or 1 (normalized instance, use_norm = 1);
+ * colbest[m] <- max_i u_ij y_i (signed, order-free); row_out[10]: [0] max
+ * |t - u.x|, [1] max |w/t|, [2] max |y|, [3] max |w/t - y|, [4] max
+ * x (p - uy)_+, [5] max |x|, [6] max (p - uy)_+, [7] rows with t <= 0,
+ * [8] sum (t - u.x)^2, [9] sum (w/t - y)^2 (fixed order). */
+int mq_pdhg_resid_rows(const mq_market *mk, const double *scales, const double *x,
+                       const double *t, const double *y, const double *p, int use_norm,
+                       double *colbest, double *row_out, double *scratch, void *stream);
+/* restart moves, row part (driver.py:242-252): out[3] = sum dt^2, sum dy^2,
+ * sum (dt - u.dx) dy over this shard. */
+int mq_pdhg_moves(const mq_market *mk, const double *xbar, const double *x0, const double *tbar,
+                  const double *t0, const double *ybar, const double *y0, double *out,
+                  double *scratch, void *stream);
+/* lifted operator power step (pdhg.py:157-161) given out_p = colsum(vx):
+ * out_y = vt - u.vx, wx = out_p[col] - u out_y[row], sums[2] = sum wx^2,
+ * sum out_y^2 (fixed order). */
+int mq_pdhg_opnorm_step(const mq_market *mk, const double *vx, const double *vt,
+                        const double *out_p, double *out_y, double *wx, double *sums,
+                        double *scratch, void *stream);
 
 /* Sparse matrix-vector product out = E p for a CSR matrix (Arrow-Debreu
  * budget map, exchange.py:89 -> sparse.py:147-153); fixed-order row sums. */

@@ -26,6 +26,7 @@ SOURCES = {
     "fast.cu": [],
     "reduce.cu": [],
     "generate.cu": [],
+    "lifted.cu": [],
     "ksection.cu": ["--fmad=false"],
 }
 

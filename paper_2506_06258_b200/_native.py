@@ -56,6 +56,15 @@ class MqState(ctypes.Structure):
 PM = ctypes.POINTER(MqMarket)
 PS = ctypes.POINTER(MqState)
 
+
+class MqLState(ctypes.Structure):
+    _fields_ = [(k, P) for k in ("x", "xbar", "t", "t_prev", "tbar", "y", "ybar", "ru",
+                                 "ru_prev", "p", "pbar", "cs", "cs_prev", "csbar", "fix",
+                                 "steps", "navg", "faults")]
+
+
+PL = ctypes.POINTER(MqLState)
+
 # name -> (restype, argtypes)
 _SIGS = {
     "mq_pdhcg_chunk": (CINT, [I64, I64, P, P, P, P, P, P, P, P, P, P, P, I64, F64, F64, CINT,
@@ -84,6 +93,14 @@ _SIGS = {
     "mq_fixed_colsum": (CINT, []),
     "mq_x_sparse": (CINT, []),
     "mq_avg_materialize": (CINT, [PM, PS, P]),
+    "mq_pdhg_step": (CINT, [PM, PL, CINT, P]),
+    "mq_pdhg_colsum_only": (CINT, [PM, PL, CINT, P]),
+    "mq_pdhg_finish_colsum": (CINT, [PM, PL, CINT, P]),
+    "mq_pdhg_chunk_end": (CINT, [PL, CINT, P]),
+    "mq_row_dot": (CINT, [PM, P, CINT, P, P]),
+    "mq_pdhg_resid_rows": (CINT, [PM, P, P, P, P, P, CINT, P, P, P, P]),
+    "mq_pdhg_moves": (CINT, [PM, P, P, P, P, P, P, P, P, P]),
+    "mq_pdhg_opnorm_step": (CINT, [PM, P, P, P, P, P, P, P, P]),
 }
 
 EXPORTED = tuple(_SIGS)

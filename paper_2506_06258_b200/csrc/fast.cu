@@ -2283,6 +2283,20 @@ int colsum_rest_launch(const mq_market *mk, const mq_state *st, int it, int fina
     return check_launch("mq_colsum_step");
 }
 
+// shared with the lifted PDHG step (lifted.cu)
+int launch_dual(const mq_market *mk, double *p, double *pbar, double *cs, double *cs_prev,
+                const double *steps, const int64_t *navg, int it, cudaStream_t s) {
+    dual_kernel<<<grid_for(mk->m, 256, sm_count() * 8), 256, 0, s>>>(mk->m, p, pbar, cs, cs_prev,
+                                                                     steps, navg, it);
+    return check_launch("mq_dual_step");
+}
+int launch_cs_from_fixed(const mq_market *mk, unsigned long long *fix, double *cs, double *csbar,
+                         const int64_t *navg, int it, cudaStream_t s) {
+    cs_from_fixed_kernel<<<grid_for(mk->m, 256, sm_count() * 8), 256, 0, s>>>(
+        mk->m, fix, cs, csbar, navg, it, 1.0 / mk->cs_scale);
+    return check_launch("mq_colsum_step");
+}
+
 int dual_launch(const mq_market *mk, const mq_state *st, int it, cudaStream_t s) {
     const int grid = grid_for(mk->m, 256, sm_count() * 8);
     dual_kernel<<<grid, 256, 0, s>>>(mk->m, st->p, st->pbar, st->cs, st->cs_prev, st->steps,

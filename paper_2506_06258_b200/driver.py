@@ -120,11 +120,17 @@ class DeviceSession:
     """Device market + engine kept alive across solves of the same utilities
     (Arrow-Debreu re-solves with new budgets; benchmarks)."""
 
-    def __init__(self, inst, cfg, group=None, dm=None):
+    def __init__(self, inst, cfg, group=None, dm=None, algo="pdhcg"):
         from .device import DeviceMarket
         from .engine import PdhcgEngine
 
         self.dm = dm if dm is not None else DeviceMarket.from_instance(inst, device=cfg.device)
+        if algo == "pdhg":  # lifted PDHG (driver.py:184-268), lifted operator norm
+            from .lifted import LiftedEngine
+
+            self.engine = LiftedEngine(self.dm, use_graphs=cfg.use_graphs, group=group)
+            self.op_norm = self.engine.op_norm()
+            return
         self.engine = PdhcgEngine(self.dm, row_solver=cfg.row_solver, sections=cfg.sections,
                                   subproblem_tol=cfg.subproblem_tol, use_graphs=cfg.use_graphs,
                                   group=group)
@@ -138,6 +144,8 @@ def solve_on_device(session, cfg, warm_start=None, w_sum=None, inst=None, algo="
     eng = session.engine
     if fingerprint is None:
         fingerprint = _Fingerprint(inst)
+    if algo == "pdhg":
+        warm_start = None  # the lifted solver ignores warm starts (driver.py:271-276)
     if warm_start is not None:
         x = np.asarray(warm_start["x"], dtype=np.float64)
         p = np.asarray(warm_start["p"], dtype=np.float64)
@@ -221,7 +229,8 @@ def solve_on_device(session, cfg, warm_start=None, w_sum=None, inst=None, algo="
         solver=algo, status=status, inner_iterations=total, restarts=restarts,
         wall_time_seconds=wall, final_residuals=final, residual_history=history,
         instance_fingerprint=fingerprint.get(),
-        config_echo=echo, subproblem_passes=passes, objective=objective,
+        config_echo=echo, subproblem_passes=None if algo == "pdhg" else passes,
+        objective=objective,
         device_stats={"chunk_seconds": chunk_time,
                       "iters_per_second": total / chunk_time if chunk_time > 0 else None,
                       "op_norm": L, "device": str(session.dm.device)},
@@ -232,19 +241,21 @@ def run_solve(inst, cfg, algo, warm_start=None):
     """Restarted solve of a Fisher instance on the GPU; returns a SolveReport.
 
     `warm_start`, when given, is a dict {"x": entry-aligned allocation,
-    "p": prices}.  Only algo="pdhcg" is provided (lifted PDHG is out of scope
-    for this hot path).
+    "p": prices} used by the compact solver; algo="pdhg" (lifted PDHG)
+    ignores it, as the reference does.
     """
-    if algo != "pdhcg":
-        if algo == "pdhg":
-            raise NotImplementedError("lifted PDHG is not part of the B200 hot path yet")
+    if algo not in ("pdhcg", "pdhg"):
         raise ValueError(f"unknown algorithm {algo!r}")
     if not isinstance(inst, FisherInstance):
         raise TypeError(f"unsupported instance type {type(inst)!r}")
+    from .device import DeviceMarket
+
     fp = _Fingerprint(inst)
-    session = DeviceSession(inst, cfg)
-    violations = device_violations(session.dm)
+    dm = DeviceMarket.from_instance(inst, device=cfg.device)
+    violations = device_violations(dm)
     if violations:
         raise ValidationError("; ".join(violations))
+    session = DeviceSession(inst, cfg, dm=dm, algo=algo)
     return solve_on_device(session, cfg, warm_start=warm_start,
-                           w_sum=float(np.sum(inst.budgets)), inst=inst, fingerprint=fp)
+                           w_sum=float(np.sum(inst.budgets)), inst=inst, fingerprint=fp,
+                           algo=algo)
