@@ -45,10 +45,10 @@
 #ifndef MQ_NSW
 #if defined(MQ_CS_DENSE)
 #define MQ_NSW 15
-#elif defined(MQ_X_DENSE) || defined(MQ_NO_XPREFETCH)
-#define MQ_NSW 19  /* no column-sum warps: 20 warps at 96 registers */
-#else
+#elif defined(MQ_XPREFETCH)
 #define MQ_NSW 18  /* + the x-prefetch warp: 20 warps at 96 registers */
+#else
+#define MQ_NSW 19  /* no column-sum warps: 20 warps at 96 registers */
 #endif
 #endif
 #ifndef MQ_NGW
@@ -534,8 +534,10 @@ static_assert(!kSparse || kAtomic, "the sparse iterate needs the fixed-point col
 // one extra warp that, a tile or two ahead of the solvers, pulls the flagged
 // (nonzero) x of each staged tile into L2 (otherwise scattered DRAM reads on
 // the solvers' critical path)
-#if !defined(MQ_NO_XPREFETCH)
-constexpr int kPF = kSparse ? 1 : 0;  // (the default MQ_NSW drops to 18 to keep 20 warps)
+// (measured +3 % while the x loads were serialized behind the price gathers;
+// no gain since they overlap, so opt-in)
+#if defined(MQ_XPREFETCH)
+constexpr int kPF = kSparse ? 1 : 0;  // (MQ_NSW should drop to 18 to keep 20 warps)
 #else
 constexpr int kPF = 0;
 #endif
@@ -1739,6 +1741,15 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         for (int pp = warp;; pp += NSW) {
             MQ_TS(tc0);
             const int rb = pp * GPW;
+#elif defined(MQ_CLAIM_AHEAD)
+        // the next claim is issued before the current pair is solved, so its
+        // shared-atomic round trip is off the critical path
+        int rb_ahead = 0;
+        if (wl == 0) rb_ahead = atomicAdd(&claim[s], GPW);
+        for (;;) {
+            MQ_TS(tc0);
+            const int rb = __shfl_sync(MQ_FULL, rb_ahead, 0);
+            if (rb < nrows && wl == 0) rb_ahead = atomicAdd(&claim[s], GPW);
 #else
         for (;;) {
             MQ_TS(tc0);
@@ -1782,24 +1793,32 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 MQ_TA(9, tc1, tq0);
                 double c[RP], u[RP];
                 uint32_t fb = 0;  // entries whose x^k was nonzero (sparse iterate)
+                // every load of the pair is issued before any is consumed: the
+                // price gathers and the flagged x loads overlap in one round trip
+                double pv[RP], xv[RP];
 #pragma unroll
                 for (int e = 0; e < RP; ++e) {
                     const int t = a + lane + e * G;
-                    if (t < b) {
-                        if (kSparse && sfl[t]) fb |= 1u << e;
-                        const double ue = su[t], xe = NGW > 0 ? 0.0 : ldxs(t);
-                        double ce;
-                        if (NGW > 0) {
-                            ce = sc[t];
-                        } else {
-                            ce = xe - tau * ld_price(st.p + scol[t]);
-                            if (x_prev_out) x_prev_out[e0 + t] = xe;
-                        }
-                        u[e] = ue;
-                        c[e] = ce;
-                    } else {
-                        u[e] = 0.0;
-                        c[e] = 0.0;
+                    const bool in = t < b;
+                    pv[e] = (in && NGW == 0) ? ld_price(st.p + scol[t]) : 0.0;
+                    bool f = false;
+                    if (kSparse) f = in && sfl[t];
+                    if (f) fb |= 1u << e;
+                    xv[e] = NGW > 0 ? 0.0
+                            : kSparse ? (f ? __ldcg(st.x + e0 + t) : 0.0)
+                                      : (in ? ldx(t) : 0.0);
+                    u[e] = in ? su[t] : 0.0;
+                }
+#pragma unroll
+                for (int e = 0; e < RP; ++e) {
+                    const int t = a + lane + e * G;
+                    c[e] = t < b ? (NGW > 0 ? sc[t] : xv[e] - tau * pv[e]) : 0.0;
+                }
+                if (x_prev_out && NGW == 0) {
+#pragma unroll
+                    for (int e = 0; e < RP; ++e) {
+                        const int t = a + lane + e * G;
+                        if (t < b) x_prev_out[e0 + t] = xv[e];
                     }
                 }
                 const double s0 = has ? ss[r] : 0.0;
