@@ -1870,19 +1870,41 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
             } else if (!kTrivial) {
                 // ---- longer rows: stream the row from shared memory
                 double s0p = 0.0, ap = 0.0, bp = 0.0;
-                for (int t = a + lane; t < b; t += G) {
-                    const double ue = su[t], xe = NGW > 0 ? 0.0 : ldxs(t);
-                    double ce;
-                    if (NGW > 0) {
-                        ce = sc[t];
-                    } else {
-                        ce = xe - tau * ld_price(st.p + scol[t]);
-                        if (x_prev_out) x_prev_out[e0 + t] = xe;
-                        sc[t] = ce;  // over x (shared stage or global): this lane's entry only
+                // batches of 8 entries per lane: all loads of a batch in flight
+                // before its c values are stored over x (the stores could alias
+                // the next loads, which would serialize every gather)
+#ifndef MQ_LB
+#define MQ_LB 8
+#endif
+                constexpr int LB = MQ_LB;
+                for (int t0 = a + lane; t0 < b; t0 += LB * G) {
+                    double pv[LB], xv[LB];
+#pragma unroll
+                    for (int q = 0; q < LB; ++q) {
+                        const int t = t0 + q * G;
+                        const bool in = t < b;
+                        pv[q] = (in && NGW == 0) ? ld_price(st.p + scol[t]) : 0.0;
+                        xv[q] = (!in || NGW > 0) ? 0.0
+                                : kSparse ? (sfl[t] ? __ldcg(st.x + e0 + t) : 0.0) : ldx(t);
                     }
-                    s0p += ue * xe;
-                    ap += ue * ce;
-                    bp += ue * ue;
+#pragma unroll
+                    for (int q = 0; q < LB; ++q) {
+                        const int t = t0 + q * G;
+                        if (t < b) {
+                            const double ue = su[t], xe = xv[q];
+                            double ce;
+                            if (NGW > 0) {
+                                ce = sc[t];
+                            } else {
+                                ce = xe - tau * pv[q];
+                                if (x_prev_out) x_prev_out[e0 + t] = xe;
+                                sc[t] = ce;  // over x (stage or global): this lane's entry only
+                            }
+                            s0p += ue * xe;
+                            ap += ue * ce;
+                            bp += ue * ue;
+                        }
+                    }
                 }
                 // with gather warps x is gone from the stage: warm start from srow
                 const double s0 = NGW > 0 ? (has ? ss[r] : 0.0) : group_sum<G>(s0p);
@@ -1892,14 +1914,27 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     row_root_exact<G>(su, sc, a, b, lane, tw, s0, A, B, has, &nsw, &ok);
                 if (has && lane == 0) st.srow[r0 + r] = sr;
                 const double inv_s = 1.0 / sr;
-                for (int t = a + lane; t < b; t += G) {
-                    const double xn = fmax(sc[t] + tw * su[t] * inv_s, 0.0);
-                    // x held c during the sweeps (direct mode): rewrite every entry
-                    put_x(t, xn, true, kXDirect);
-                    if (!kSparse) __stcs(st.xbar + e0 + t, av.wold * ldxb(t) + av.wnew * xn);
-                    if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
-                    if (kBucket) st_keep(bslot + stp[t], xn, pkeep);
-                    if (kAtomic && xn > 0.0) fixed_colsum_add(mk, st, scol[t], xn);
+                for (int t0 = a + lane; t0 < b; t0 += LB * G) {
+                    double cv[LB];
+#pragma unroll
+                    for (int q = 0; q < LB; ++q) {
+                        const int t = t0 + q * G;
+                        cv[q] = t < b ? sc[t] : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < LB; ++q) {
+                        const int t = t0 + q * G;
+                        if (t < b) {
+                            const double xn = fmax(cv[q] + tw * su[t] * inv_s, 0.0);
+                            // x held c during the sweeps (direct mode): rewrite every entry
+                            put_x(t, xn, true, kXDirect);
+                            if (!kSparse)
+                                __stcs(st.xbar + e0 + t, av.wold * ldxb(t) + av.wnew * xn);
+                            if (kScatter) st_keep(st.xc + stp[t], xn, pkeep);
+                            if (kBucket) st_keep(bslot + stp[t], xn, pkeep);
+                            if (kAtomic && xn > 0.0) fixed_colsum_add(mk, st, scol[t], xn);
+                        }
+                    }
                 }
                 // c was written over x in this stage: order those generic-proxy
                 // writes before the producer's next bulk copy into the stage

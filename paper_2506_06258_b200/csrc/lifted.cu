@@ -55,13 +55,21 @@ pdhg_rows_kernel(const mq_market mk, const mq_lstate ls, int it) {
         const double root = sqrt(d * d + 4.0 * tau * wi);
         const double tn = d > 0.0 ? 2.0 * tau * wi / (d + root) : 0.5 * (root - d);
         double acc = 0.0;
+        // restrict-qualified views: loads of later entries may be issued
+        // before the stores of earlier ones (no aliasing between the arrays)
+        double *__restrict__ X = ls.x;
+        double *__restrict__ XB = ls.xbar;
+        const double *__restrict__ P = ls.p;
+        const double *__restrict__ U = mk.u;
+        const int32_t *__restrict__ C = mk.col;
+#pragma unroll 4
         for (int64_t e = a + lane; e < b; e += 32) {  // kernels.py:182-185
-            const int j = mk.col[e];
-            const double ue = mk.u[e];
-            const double xv = ls.x[e] - tau * (ls.p[j] - ue * yi);
+            const int j = C[e];
+            const double ue = U[e];
+            const double xv = X[e] - tau * (__ldg(P + j) - ue * yi);
             const double xn = xv > 0.0 ? xv : 0.0;
-            ls.x[e] = xn;
-            ls.xbar[e] = av.wold * ls.xbar[e] + av.wnew * xn;
+            X[e] = xn;
+            XB[e] = av.wold * XB[e] + av.wnew * xn;
             acc += ue * xn;
             if (xn > 0.0) fix_add(mk, ls.fix, ls.faults, j, xn);
         }
