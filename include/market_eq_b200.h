@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define MQ_ABI_VERSION 4
+#define MQ_ABI_VERSION 5
 #define MQ_TILE_ENTRIES 3584 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
@@ -55,32 +55,18 @@ typedef struct mq_market {
     int64_t ntiles;
     const int32_t *long_rows; /* rows longer than MQ_LONG_ROW                   */
     int64_t nlong;
-    /* tile-blocked transpose schedule for the fused column sums: the tiles
-       are grouped in blocks of tiles_per_block consecutive tiles (block b is
-       finished once the persistent grid of prim_grid CTAs has solved it);
-       bperm lists, block by block and column by column, the entry positions
-       of each block (ascending inside a column), bptr[b*m + j] where
-       (block b, good j) starts; pseudo-block nblk holds the long rows'
-       entries.  Walking a good's segments over b = 0..nblk visits its tile
-       entries in ascending row order.                                        */
+    /* tile-blocked transpose schedule of the deterministic fp64 column sums
+       (mq_colsum: residual checks, restarts): the tiles are grouped in blocks
+       of tiles_per_block consecutive tiles; bperm lists, block by block and
+       column by column, the entry positions of each block (ascending inside
+       a column), bptr[b*m + j] where (block b, good j) starts; pseudo-block
+       nblk holds the long rows' entries.                                     */
     const int32_t *bperm;    /* [nnz]                                           */
     const int32_t *bptr;     /* [(nblk+1)*m + 1]                                */
     int64_t nblk, tiles_per_block;
     int32_t prim_grid;       /* CTAs of the persistent primal kernel            */
-    /* column-major positions (scatter mode): entry e is the tpos[e]-th entry
-       of the reference's transpose schedule (sparse.py:130-145); good j owns
-       positions [tptr[j], tptr[j+1]) of that order                           */
-    const int32_t *tpos;     /* [nnz] [pad]                                     */
-    const int64_t *tptr;     /* [m+1]                                           */
     int64_t row_begin;       /* first global row of this shard (0 on 1 GPU)    */
-    /* bucketed column sums (default build): entry e of block b is the
-       bpos[e]-th entry of the block's bperm order; the primal kernel stores
-       x_e there in an L2-resident bucket of bcap doubles (one of
-       mq_bucket_slots() rotating buckets), the column-sum warps then read each
-       good's segment contiguously                                             */
-    const int32_t *bpos;     /* [nnz] [pad]                                     */
-    int64_t bcap;            /* entries of the largest block                    */
-    /* fixed-point column sums (default build, mq_colsum_mode() == 5): x_e is
+    /* fixed-point column sums of the price step: x_e is
        added to its good's u64 accumulator as round(x_e * cs_scale) when
        0 < x_e < cs_xmax (larger values count as faults); cs_scale = 2^k with
        cs_xmax * cs_scale * (max entries of a good) <= 2^62                    */
@@ -99,21 +85,18 @@ typedef struct mq_state {
     double *cs;       /* [m]   colsum(x^k)                                     */
     double *cs_prev;  /* [m]   colsum(x^{k-1})                                 */
     double *csbar;    /* [m]   colsum(xbar)                                    */
-    int32_t *blk_done;/* [2*nblk+1] per block: tiles solved, column sums done;
-                         then the dynamic tile counter (zeroed per launch)     */
-    double *xc;       /* [nnz] x in column-major order (scatter mode)          */
+    int32_t *blk_done;/* [1] the primal kernel's dynamic tile counter         */
     const double *steps; /* [2] tau, sigma (device-resident: one graph serves
                             every step size)                                   */
     int64_t *navg;    /* [1]  inner iterations since the last restart          */
     int64_t *pass_out;/* [iters] per-iteration row-solver work counter         */
     int64_t *faults;  /* [1]  rows whose solver failed                         */
-    double *bucket;   /* column-sum scratch: mq_bucket_slots() * bcap doubles
-                         (bucket mode) or m u64 accumulators (fixed-point mode,
-                         zero between iterations)                              */
+    double *bucket;   /* [m] u64 fixed-point column-sum accumulators (zero
+                         between iterations)                                   */
     double *srow;     /* [n] [pad] per-buyer utility after the last prox: the
                          row solve's warm start (<= 0: none; any value is
                          correct, a close one saves sweeps)                    */
-    /* sparse iterate (mq_x_sparse() == 1): xflag[e] = (x[e] > 0) is staged
+    /* sparse iterate: xflag[e] = (x[e] > 0) is staged
        instead of x (x is read only where flagged and stays exact); xsum =
        sum of x since the last restart, xbar = xsum / navg is written by
        mq_avg_materialize.  The host sets xflag = 1 and xsum = navg * xbar
@@ -276,12 +259,9 @@ int mq_gen_fill(int64_t row0, int64_t nrows, int64_t m, int q_mode, double q, do
  * it; MQ_TILE_ENTRIES by default). */
 int mq_tile_entries(void);
 
-/* How this build computes the price step's column sums: 0 = gathered from L2
- * inside the persistent primal kernel by column-sum warps, 1 = scattered by
- * mq_primal_step into st->xc (column-major, needs mk->tpos / mk->tptr) and
- * streamed by mq_colsum_step, 2 (default) = per block of tiles, a primal
- * launch followed by a gather launch over the block's schedule while its x is
- * L2-resident. */
+/* How this build computes the price step's column sums: 5 = fixed-point
+ * atomics on the nonzero entries (the only mode of this build; the earlier
+ * gathered / scattered / bucketed modes are described in DESIGN.md §11). */
 int mq_colsum_mode(void);
 
 /* Size in doubles of the `scratch` buffer the reduction calls need. */
@@ -289,8 +269,6 @@ int64_t mq_scratch_doubles(void);
 
 const char *mq_last_error(void);
 int mq_abi_version(void);
-/* rotating column-sum buckets the build needs (0: none) */
-int mq_bucket_slots(void);
 /* 1 if the build sums columns in fixed point (state.bucket = m u64) */
 int mq_fixed_colsum(void);
 /* 1 if the build keeps the sparse iterate (xflag / xsum) */

@@ -17,7 +17,7 @@ TILE_ENTRIES = 3584   # MQ_TILE_ENTRIES
 LONG_ROW = 1024       # MQ_LONG_ROW
 TILE_ROWS = 256       # MQ_TILE_ROWS
 PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 _lock = threading.Lock()
 _lib = None
@@ -41,14 +41,13 @@ class MqMarket(ctypes.Structure):
                 ("row_ptr", P), ("col", P), ("u", P), ("u_orig", P), ("w", P),
                 ("tiles", P), ("ntiles", I64), ("long_rows", P), ("nlong", I64),
                 ("bperm", P), ("bptr", P), ("nblk", I64), ("tiles_per_block", I64),
-                ("prim_grid", ctypes.c_int32), ("tpos", P), ("tptr", P), ("row_begin", I64),
-                ("bpos", P), ("bcap", I64), ("cs_scale", ctypes.c_double),
-                ("cs_xmax", ctypes.c_double)]
+                ("prim_grid", ctypes.c_int32), ("row_begin", I64),
+                ("cs_scale", ctypes.c_double), ("cs_xmax", ctypes.c_double)]
 
 
 class MqState(ctypes.Structure):
     _fields_ = [("x", P), ("xbar", P), ("p", P), ("pbar", P), ("cs", P), ("cs_prev", P),
-                ("csbar", P), ("blk_done", P), ("xc", P), ("steps", P), ("navg", P),
+                ("csbar", P), ("blk_done", P), ("steps", P), ("navg", P),
                 ("pass_out", P), ("faults", P), ("bucket", P), ("srow", P),
                 ("xflag", P), ("xsum", P)]
 
@@ -89,7 +88,6 @@ _SIGS = {
     "mq_colsum_mode": (CINT, []),
     "mq_last_error": (ctypes.c_char_p, []),
     "mq_abi_version": (CINT, []),
-    "mq_bucket_slots": (CINT, []),
     "mq_fixed_colsum": (CINT, []),
     "mq_x_sparse": (CINT, []),
     "mq_avg_materialize": (CINT, [PM, PS, P]),

@@ -87,39 +87,15 @@ def build_tiles(row_ptr, tile_entries=nat.TILE_ENTRIES, long_row=nat.LONG_ROW,
 TILES_PER_CTA_PER_BLOCK = int(os.environ.get("MQ_TILES_PER_CTA", "4"))  # tuning override
 
 
-def build_transpose(col, m):
-    """(tpos int32 [nnz + pad], tptr int64 [m+1]): column-major position of
-    every entry under the stable column grouping of sparse.py:130-145."""
-    dev = col.device
-    nnz = col.numel()
-    tpos = torch.zeros(nnz + nat.PAD, dtype=torch.int32, device=dev)
-    if nnz:
-        _, perm = torch.sort(col, stable=True)
-        tpos[:nnz].scatter_(0, perm, torch.arange(nnz, dtype=torch.int32, device=dev))
-        del perm
-    counts = (torch.bincount(col.to(torch.int64), minlength=m) if nnz
-              else torch.zeros(m, dtype=torch.int64, device=dev))
-    tptr = torch.zeros(m + 1, dtype=torch.int64, device=dev)
-    torch.cumsum(counts, 0, out=tptr[1:])
-    return tpos, tptr
-
-
 def sm_count(device):
     return torch.cuda.get_device_properties(device).multi_processor_count
 
 
-SPLIT_TILES_PER_BLOCK = 2048   # colsum modes 2/3: ~4M entries (32 MB of x) per block
-
-
 def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
-                           tiles_per_cta=TILES_PER_CTA_PER_BLOCK, tiles_per_block=None,
-                           with_bpos=False):
+                           tiles_per_cta=TILES_PER_CTA_PER_BLOCK, tiles_per_block=None):
     """Entry positions grouped by (block of tiles, good), ascending inside a
     good; long-row entries form the last pseudo-block.  Returns
-    (bperm int32 [nnz], bptr int32 [(nblk+1)*m+1], nblk, tiles_per_block,
-    bpos, bcap): with with_bpos, bpos int32 [nnz + pad] is the inverse of
-    bperm relative to the entry's block start (its slot in the block's
-    column-sum bucket) and bcap the largest tile block; else (None, 0)."""
+    (bperm int32 [nnz], bptr int32 [(nblk+1)*m+1], nblk, tiles_per_block)."""
     dev = col.device
     nnz = col.numel()
     ntiles = int(tiles.shape[0])
@@ -146,8 +122,7 @@ def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
         key = blk.to(torch.int32) * m + col
     else:
         key = blk * m + col.to(torch.int64)
-    if not with_bpos:
-        del blk
+    del blk
     _, perm = torch.sort(key, stable=True)
     # [pad]: the fused kernel stages slices of both arrays with TMA bulk copies
     bperm = torch.zeros(nnz + nat.PAD, dtype=torch.int32, device=dev)
@@ -159,20 +134,7 @@ def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
     torch.cumsum(counts, 0, out=bptr[1:])
     bptr32 = torch.zeros(total + 1 + nat.PAD, dtype=torch.int32, device=dev)
     bptr32[:total + 1] = bptr
-    bpos, bcap = None, 0
-    if with_bpos:
-        bpos = torch.zeros(nnz + nat.PAD, dtype=torch.int32, device=dev)
-        if nnz:
-            bpos[:nnz].scatter_(0, bperm[:nnz].to(torch.int64),
-                                torch.arange(nnz, dtype=torch.int32, device=dev))
-            base = bptr[torch.arange(nblk + 1, device=dev) * m]  # block starts
-            bpos[:nnz] -= base[blk].to(torch.int32)
-        del blk
-        if nblk:
-            ext = bptr[torch.arange(1, nblk + 1, device=dev) * m] - bptr[
-                torch.arange(nblk, device=dev) * m]
-            bcap = -(-int(ext.max().item()) // 16) * 16  # buckets stay 128-byte aligned
-    return bperm[:nnz], bptr32[:total + 1], nblk, tpb, bpos, bcap
+    return bperm[:nnz], bptr32[:total + 1], nblk, tpb
 
 
 def fixed_point_scale(max_col_count):
@@ -240,21 +202,15 @@ class DeviceMarket:
             # (r0, r1, e0, e1) per tile: the producer warp needs no dependent loads
             self.tiles = torch.cat([tiles2, self.row_ptr[tiles2]], 1).contiguous()
             self.prim_grid = int(min(max(1, self.tiles.shape[0]), sm_count(dev)))
-            mode = int(self.lib.mq_colsum_mode())
-            (self.bperm, self.bptr, self.nblk, self.tiles_per_block, self._bpos,
-             self.bcap) = build_blocked_schedule(
-                self.row_ptr, self.col, self.m, tiles2, self.long_rows, self.prim_grid,
-                tiles_per_block=SPLIT_TILES_PER_BLOCK if mode in (2, 3) else None,
-                with_bpos=mode == 4)
+            # the blocked schedule orders the deterministic fp64 column sums of
+            # the residual checks (mq_colsum)
+            self.bperm, self.bptr, self.nblk, self.tiles_per_block = build_blocked_schedule(
+                self.row_ptr, self.col, self.m, tiles2, self.long_rows, self.prim_grid)
             self.max_col_count = int(self.col_counts.max().item()) if self.m else 0
             lens = self.row_ptr[1:] - self.row_ptr[:-1]
             self.max_row_len = int(lens.max().item()) if self.n else 0
         self.tperm = self.tptr = None
         self.colsum_mode = int(self.lib.mq_colsum_mode())
-        self._tpos = self._tptr_c = None
-        if self.colsum_mode == 1:
-            with torch.cuda.device(dev):
-                self._tpos, self._tptr_c = build_transpose(self.col, self.m)
         self.struct = self._make_struct()
 
     def global_schedule(self):
@@ -285,13 +241,7 @@ class DeviceMarket:
         s.nblk = int(self.nblk)
         s.tiles_per_block = int(self.tiles_per_block)
         s.prim_grid = int(self.prim_grid)
-        if self._tpos is not None:
-            s.tpos = self._tpos.data_ptr()
-            s.tptr = self._tptr_c.data_ptr()
         s.row_begin = self.row_begin
-        if self._bpos is not None:
-            s.bpos = self._bpos.data_ptr()
-        s.bcap = int(self.bcap)
         s.cs_scale, s.cs_xmax = fixed_point_scale(self.max_col_count)
         return s
 

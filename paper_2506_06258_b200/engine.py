@@ -215,19 +215,12 @@ class PdhcgEngine:
         # per-buyer utility of the last prox: the fused row solve's warm start
         self._srow_buf = torch.zeros(dm.n + nat.PAD, **f64)
         self.srow = self._srow_buf[:dm.n]
-        # per block: tiles solved, then column-sum warps done (throttle)
-        self.blk_done = torch.zeros(2 * dm.nblk + 1, dtype=torch.int32, device=dev)
-        # column-major copy of x (only for a scatter-mode build)
-        self.xc = torch.zeros(nnz if getattr(dm, "colsum_mode", 0) == 1 else 1, **f64)
-        # column-sum buckets (bucket-mode build): L2-resident scratch
-        slots = int(dm.lib.mq_bucket_slots()) if hasattr(dm, "lib") else 0
-        nb = slots * int(getattr(dm, "bcap", 0))
+        # the primal kernel's dynamic tile counter
+        self.blk_done = torch.zeros(1, dtype=torch.int32, device=dev)
+        # fixed-point column sums: m u64 accumulators, zero between iterations
         fixed = getattr(getattr(dm, "lib", None), "mq_fixed_colsum", None)
-        # fixed-point column sums (default build): m u64 accumulators
         self.fixed = bool(fixed is not None and fixed() == 1 and self.mode != "ksection")
-        if self.fixed:
-            nb = max(nb, m)
-        self.bucket = torch.zeros(max(1, nb), **f64)
+        self.bucket = torch.zeros(max(1, m if self.fixed else 1), **f64)
         self.p = torch.zeros(m, **f64)
         self.pbar = torch.zeros(m, **f64)
         self.p0 = torch.zeros(m, **f64)
@@ -267,7 +260,7 @@ class PdhcgEngine:
         if not isinstance(self.ops, NativeOps):
             return None
         s = nat.MqState()
-        for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "blk_done", "xc",
+        for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "blk_done",
                      "steps", "faults", "srow", "bucket", "xflag", "xsum"):
             setattr(s, name, getattr(self, name).data_ptr())
         s.navg = self.navg_dev.data_ptr()

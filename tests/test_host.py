@@ -24,7 +24,7 @@ def test_native_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(lib, name)
-    assert lib.mq_abi_version() == 4
+    assert lib.mq_abi_version() == 5
     assert lib.mq_scratch_doubles() > 0
 
 
@@ -174,7 +174,6 @@ def test_abi_marshaling_without_device():
         "mq_gen_degrees": (0, 1, 10, 0, 0.5, 2.0, 1.0, 1, None, None),
         "mq_tile_entries": (),
         "mq_colsum_mode": (),
-        "mq_bucket_slots": (),
         "mq_fixed_colsum": (),
         "mq_x_sparse": (),
         "mq_avg_materialize": (mk, st, None),
@@ -187,7 +186,7 @@ def test_abi_marshaling_without_device():
         if name == "mq_colsum_mode":
             assert rc in (0, 1, 2, 3, 4, 5)
             continue
-        if name in ("mq_bucket_slots", "mq_fixed_colsum", "mq_x_sparse"):
+        if name in ("mq_fixed_colsum", "mq_x_sparse"):
             assert rc >= 0
             continue
         assert rc != 0, name
@@ -245,16 +244,10 @@ def test_blocked_schedule_preserves_column_order():
     rp, col = _random_csr(rng, n, m, lens)
     rpt = torch.from_numpy(rp)
     tiles, long_rows = build_tiles(rpt, 64, 30, 16)
-    bperm, bptr, nblk, tpb, bpos, bcap = build_blocked_schedule(
+    bperm, bptr, nblk, tpb = build_blocked_schedule(
         rpt, torch.from_numpy(col.astype(np.int32)), m, tiles, long_rows, prim_grid=3,
-        tiles_per_cta=2, with_bpos=True)
-    bperm, bptr, bpos = bperm.numpy(), bptr.numpy(), bpos.numpy()[:len(col)]
-    # bpos: each entry's slot in its block's bucket (inverse of bperm, block-relative)
-    starts = bptr[np.arange(nblk + 1) * m]
-    assert bcap == -(-int(np.max(np.diff(starts))) // 16) * 16  # largest tile block, rounded
-    for b in range(nblk + 1):
-        seg = bperm[starts[b]:(starts[b + 1] if b < nblk else len(col))]
-        assert np.array_equal(bpos[seg], np.arange(len(seg)))
+        tiles_per_cta=2)
+    bperm, bptr = bperm.numpy(), bptr.numpy()
     assert tpb == 6 and nblk == -(-tiles.shape[0] // 6)
     assert np.array_equal(np.sort(bperm), np.arange(len(col)))
     row_of = np.repeat(np.arange(n), np.diff(rp))

@@ -29,12 +29,17 @@ lib.mq_debug_counters(buf)
 ms = e0.elapsed_time(e1) / 10
 cyc = ms * 1e-3 * 1.965e9
 nsm = dm.prim_grid
-names = ["solver wait tile", "solver throttled", "producer wait stage", "colsum wait block",
-         "colsum gather", "solver pass1", "solver root", "solver write", "solver claim",
+names = ["solver wait tile", "(unused)", "producer wait stage", "(unused)", "(unused)",
+         "solver loads + c", "solver root", "solver stores", "solver claim",
          "solver row meta", "solver tile end"]
 print(f"{cfg}: {ms:.3f} ms/iter, kernel-cycles/SM ~{cyc:.3e}")
-per_warp = {0: 15, 1: 15, 2: 1, 3: 4, 4: 4, 5: 15, 6: 15, 7: 15, 8: 15, 9: 15, 10: 15}
+NSW = 19  # solver warps of the default build (fast.cu MQ_NSW)
+per_warp = {i: NSW for i in range(11)}
+per_warp[2] = 1
 for i, nm in enumerate(names):
+    if nm == "(unused)":
+        continue
     v = buf[i] / 10 / nsm / per_warp[i]
     print(f"  {nm:22s} {v:.3e} cycles per warp per iter ({100 * v / cyc:.1f}% of iter)")
-print(f"  row pairs per warp per iter {buf[12] / 10 / nsm / 15:.0f}, tile visits {buf[13] / 10 / nsm / 15:.0f}")
+print(f"  row pairs per warp per iter {buf[12] / 10 / nsm / NSW:.0f}, "
+      f"tile visits {buf[13] / 10 / nsm / NSW:.0f}")

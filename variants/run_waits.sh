@@ -1,3 +1,4 @@
+# wait-cycle breakdown of every variants/lib_w_*.so (built with MQ_PROFILE_WAITS)
 mkdir -p gpurun_out
 for v in variants/lib_w_*.so; do
   n=$(basename $v .so)
