@@ -33,7 +33,7 @@ extern "C" {
 #endif
 
 #define MQ_ABI_VERSION 5
-#define MQ_TILE_ENTRIES 3584 /* entries staged per shared-memory tile (default build) */
+#define MQ_TILE_ENTRIES 2560 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
 

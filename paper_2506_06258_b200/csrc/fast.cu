@@ -25,7 +25,7 @@
 // One persistent, warp-specialized kernel per iteration (primal_fused_kernel):
 //  * a TMA producer warp streams each tile (whole rows, <= MQ_TILE_ENTRIES
 //    entries: u, col, flags, row offsets, budgets, warm starts) into a
-//    3-stage shared-memory ring with cp.async.bulk + mbarrier transaction
+//    4-stage shared-memory ring with cp.async.bulk + mbarrier transaction
 //    counts, claiming tiles dynamically from a global counter;
 //  * 19 solver warps claim row pairs of the current tile (two 16-lane groups
 //    per warp) and solve them, rows of <= 128 entries in registers.
@@ -48,7 +48,7 @@
 // (p[col]) need L1 lines to track their misses, and their throughput halves
 // when the carveout leaves ~28 KB (tools/micro/gather_l1.cu).
 #ifndef MQ_STAGES
-#define MQ_STAGES 3
+#define MQ_STAGES 4  // 4 x 2560-entry stages: 158 KB (carveout 164 KB, 92 KB of L1)
 #endif
 #ifndef MQ_REG_PER
 #define MQ_REG_PER 8  // entries per lane kept in registers (rows <= MQ_G * MQ_REG_PER)

@@ -1,4 +1,4 @@
-# usage: bash variants/sweep.sh "lib_name[:ENV=V ...]" ...
+# usage: bash variants/sweep.sh "lib_name[:ENV=V ...]" ...  -> config-4 it/s per variant
 mkdir -p gpurun_out
 for spec in "$@"; do
   lib=${spec%%:*}; envs=""; [ "$spec" != "$lib" ] && envs=${spec#*:}
