@@ -151,13 +151,16 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+// The fire-and-forget stores below carry no "memory" clobber: nothing in the
+// kernel reads these addresses after writing them, and without the compiler
+// barrier the loads around them (staged columns, utilities) can be scheduled
+// freely.
 __device__ __forceinline__ void st_flag(uint8_t *p, bool v) {
-    asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"((int)v) : "memory");
+    asm volatile("st.global.u8 [%0], %1;" ::"l"(p), "r"((int)v));
 }
-// fire-and-forget float add (one writer per address and iteration: the
-// result is the plain rounded sum, deterministic)
+// float add (one writer per address and iteration: the plain rounded sum)
 __device__ __forceinline__ void red_add_f64(double *p, double v) {
-    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v));
 }
 // 16-byte-aligned superset of [first, first+count) elements of size S
 template <int S>
@@ -177,8 +180,7 @@ __device__ __forceinline__ void fixed_colsum_add(const mq_market &mk, const mq_s
     if (xe < mk.cs_xmax) {
         asm volatile("red.global.add.u64 [%0], %1;" ::"l"(reinterpret_cast<unsigned long long *>(
                          st.bucket) + j),
-                     "l"(__double2ull_rn(xe * mk.cs_scale))
-                     : "memory");
+                     "l"(__double2ull_rn(xe * mk.cs_scale)));
     } else {
         atomicAdd(reinterpret_cast<unsigned long long *>(st.faults), 1ull);
     }
