@@ -142,22 +142,21 @@ int mq_pdhcg_chunk(int64_t n, int64_t m, const int64_t *indptr, const int32_t *c
  * p += sigma (2 cs - cs_prev - 1); pbar <- avg; cs_prev <- cs. */
 int mq_dual_step(const mq_market *mk, const mq_state *st, int it, void *stream);
 
-/* Exact per-buyer proximal step fused with the allocation average and the
+/* Exact per-buyer proximal step fused with the running average and the
  * column sums (kernels.py:117-142 then the next iteration's 111-116): for
  * every row, the unique root s of s = sum_j u_j max(0, c_j + tau w u_j / s),
  * c = x - tau p[col], by the monotone active-set iteration (closed-form root
- * per active set), then x <- max(0, c + tau w u / s), xbar <- avg; the
- * kernel's column-sum warps gather each finished block of x from L2 into
- * cs = colsum(x) over the tile rows (deterministic: one thread per good,
- * blocks in order).  x_prev_out (may be NULL) receives the pre-step x (the
- * reference's x_prev copy).  pass_out[it] += number of active-set sweeps. */
+ * per active set, warm-started from srow), then x <- max(0, c + tau w u / s)
+ * with its flag, the running sum xsum and the fixed-point column-sum atomics
+ * of the nonzero entries.  x_prev_out (may be NULL) receives the pre-step x
+ * (the reference's x_prev copy).  pass_out[it] += number of sweeps. */
 int mq_primal_step(const mq_market *mk, const mq_state *st, int it, double *x_prev_out,
                    void *stream);
 
-/* Completes cs = colsum(x) over this shard: adds the long rows' entries (the
- * pseudo-block of the schedule) to the tile sums of mq_primal_step.  With
- * finalize != 0 (single GPU) also csbar <- avg(csbar, cs); multi-GPU callers
- * allreduce cs first and then call mq_colsum_finalize. */
+/* cs = colsum(x) over this shard from the fixed-point accumulators (which it
+ * zeroes).  With finalize != 0 also csbar <- avg(csbar, cs); multi-GPU callers
+ * all-reduce the accumulators (int64) first and then call it with
+ * finalize != 0; mq_colsum_finalize updates csbar alone. */
 int mq_colsum_step(const mq_market *mk, const mq_state *st, int it, int finalize,
                    void *stream);
 int mq_colsum_finalize(const mq_market *mk, const mq_state *st, int it, void *stream);
@@ -165,7 +164,8 @@ int mq_colsum_finalize(const mq_market *mk, const mq_state *st, int it, void *st
 /* navg += iters (end of a captured chunk). */
 int mq_chunk_end(const mq_state *st, int iters, void *stream);
 
-/* Whole chunk on one GPU: `iters` x (dual, primal, colsum) + chunk_end. */
+/* Whole chunk on one GPU: `iters` x (dual, primal, colsum) + chunk_end +
+ * mq_avg_materialize. */
 int mq_fast_chunk(const mq_market *mk, const mq_state *st, int iters, void *stream);
 
 /* Plain column sums out[j] = sum_{col j} v over this shard, one thread per
