@@ -230,6 +230,19 @@ int mq_pdhg_opnorm_step(const mq_market *mk, const double *vx, const double *vt,
                         const double *out_p, double *out_y, double *wx, double *sums,
                         double *scratch, void *stream);
 
+/* ---- theory diagnostics (kkt.py:88-168) ---------------------------------
+ * Scaled KKT residual, row/entry parts on the original utilities: out[4] =
+ * sum (t y - w)^2, sum (x - [x - slack/xi]_+)^2, sum min(slack, 0)^2,
+ * sum (t - u.x)^2 with slack = p_j - u_ij y_i (fixed order). */
+int mq_scaled_kkt_rows(const mq_market *mk, const double *x, const double *t, const double *p,
+                       const double *y, double xi, double *out, double *scratch, void *stream);
+/* Smoothed gap, allocation part: out[0] = sum_i -w_i log(u_i.xh_i) + p.xh_i +
+ * xi/2 |xh_i - xc_i|^2 with xh_i the exact row prox of (xc, p) at step 1/xi
+ * (cbuf: nnz scratch); rows whose iteration did not settle add to *faults. */
+int mq_smoothed_gap_rows(const mq_market *mk, const double *xc, const double *p, double xi,
+                         double *cbuf, double *out, double *scratch, int64_t *faults,
+                         void *stream);
+
 /* Sparse matrix-vector product out = E p for a CSR matrix (Arrow-Debreu
  * budget map, exchange.py:89 -> sparse.py:147-153); fixed-order row sums. */
 int mq_spmv(int64_t n_rows, const int64_t *row_ptr, const int32_t *col,

@@ -13,6 +13,7 @@ Fixtures (all float64 stored exactly):
   rowroot.npz    rows  -> kernels._row_root                      (row-solver vectors)
   solve_*.npz    instance -> run_solve(...) report               (full solves)
   pdhg_*.npz     instance -> run_solve(..., "pdhg") report       (lifted PDHG solves)
+  theory.npz     random states -> kkt.scaled_kkt_residual(_compact), kkt.smoothed_gap
   resid.npz      random states -> kkt.residuals_compact           (residual formulas)
   exchange.npz   generate_exchange -> solve_exchange trace       (Arrow-Debreu)
   gen.json       generator fingerprints (instance_fingerprint)   (generator parity)
@@ -261,6 +262,35 @@ def pdhg_cases():
     pdhg_case("g80_theory", g, me.SolveConfig(tol=1e-3, step_mode="theory", max_iters=6000))
 
 
+def theory_case():
+    """kkt.py:88-168 diagnostics on random states of two generated markets."""
+    out = {}
+    rng = np.random.default_rng(7)
+    for tag, cfg in (("a", me.GeneratorConfig(n=60, m=25, sparsity_u=0.3, seed=11)),
+                     ("b", me.GeneratorConfig(n=200, m=80, sparsity_u=0.2, seed=1))):
+        inst = me.generate_fisher(cfg)
+        u = inst.utilities
+        out[f"{tag}_indptr"], out[f"{tag}_col"] = u.row_offsets, u.col_indices
+        out[f"{tag}_u"], out[f"{tag}_w"] = u.values, inst.budgets
+        out[f"{tag}_nm"] = np.array([u.n_rows, u.n_cols])
+        for k in range(3):
+            x = rng.random(u.nnz) * 0.1
+            t = rng.random(u.n_rows) + 0.1
+            p = rng.random(u.n_cols) + 0.05
+            y = rng.random(u.n_rows) * 2.0 - 0.2
+            xc = rng.random(u.nnz) * 0.1
+            pc = rng.random(u.n_cols) + 0.05
+            xi = [0.5, 1.0, 3.0][k]
+            out[f"{tag}{k}_x"], out[f"{tag}{k}_t"], out[f"{tag}{k}_p"] = x, t, p
+            out[f"{tag}{k}_y"], out[f"{tag}{k}_xc"], out[f"{tag}{k}_pc"] = y, xc, pc
+            out[f"{tag}{k}_xi"] = np.float64(xi)
+            out[f"{tag}{k}_skkt"] = np.float64(me.kkt.scaled_kkt_residual(inst, x, t, p, y, xi))
+            out[f"{tag}{k}_skkt_c"] = np.float64(me.kkt.scaled_kkt_residual_compact(inst, x, p, xi))
+            out[f"{tag}{k}_gap"] = np.float64(me.kkt.smoothed_gap(inst, (x, p), (xc, pc), xi=xi))
+            print(f"  theory {tag}{k}: skkt={out[f'{tag}{k}_skkt']!r} gap={out[f'{tag}{k}_gap']!r}")
+    save("theory.npz", **out)
+
+
 def c1_instance():
     """BASELINE config 1: dense 1000x500, U~U(0,1) (default_rng(0)), w=1."""
     U = np.random.default_rng(0).random((1000, 500))
@@ -411,7 +441,7 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     orc.set_threads(os.cpu_count())
     steps = {"chunk": chunk_cases, "rowroot": rowroot_cases, "solve": lambda: solve_cases(a.big),
-             "pdhg": pdhg_cases,
+             "pdhg": pdhg_cases, "theory": theory_case,
              "bigsolve": big_solve_cases,
              "resid": resid_cases, "exchange": exchange_case,
              "gen": lambda: gen_fingerprints(a.big), "c2": c2_lockstep}

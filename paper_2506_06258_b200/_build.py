@@ -27,6 +27,7 @@ SOURCES = {
     "reduce.cu": [],
     "generate.cu": [],
     "lifted.cu": [],
+    "theory.cu": [],
     "ksection.cu": ["--fmad=false"],
 }
 

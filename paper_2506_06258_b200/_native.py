@@ -99,6 +99,8 @@ _SIGS = {
     "mq_pdhg_resid_rows": (CINT, [PM, P, P, P, P, P, CINT, P, P, P, P]),
     "mq_pdhg_moves": (CINT, [PM, P, P, P, P, P, P, P, P, P]),
     "mq_pdhg_opnorm_step": (CINT, [PM, P, P, P, P, P, P, P, P]),
+    "mq_scaled_kkt_rows": (CINT, [PM, P, P, P, P, F64, P, P, P]),
+    "mq_smoothed_gap_rows": (CINT, [PM, P, P, F64, P, P, P, P, P]),
 }
 
 EXPORTED = tuple(_SIGS)

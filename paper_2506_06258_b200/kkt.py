@@ -47,3 +47,94 @@ def residuals_compact(inst, x, p):
 def eg_objective(inst, x):
     """-sum_i w_i log(u_i . x_i); +inf if some buyer has zero utility."""
     return _engine_for(inst, x).final_payload()["objective"]
+
+
+# ------------------------------------------------------------ theory diagnostics
+def _dev(a, dm, dtype=None):
+    import numpy as np
+    import torch
+
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dm.device)
+
+
+def scaled_kkt_residual(inst, x, t, p, y, xi=1.0):
+    """Euclidean norm of the stacked scaled KKT residual (kkt.py:88-111):
+    t_i y_i - w_i, x_ij - [x_ij - (p_j - u_ij y_i)/xi]_+, [p_j - u_ij y_i]_-,
+    colsum(x) - 1 and t_i - u_i.x_i, computed on the device."""
+    import math
+
+    import torch
+
+    from . import _native as nat
+    from .device import DeviceMarket
+    from .engine import _cur_stream
+
+    if xi <= 0:
+        raise ValueError("xi must be positive")
+    dm = DeviceMarket.from_instance(inst)
+    xd, td, pd, yd = (_dev(a, dm) for a in (x, t, p, y))
+    out = torch.zeros(4, dtype=torch.float64, device=dm.device)
+    scratch = torch.zeros(int(dm.lib.mq_scratch_doubles()), dtype=torch.float64,
+                          device=dm.device)
+    nat.check(dm.lib.mq_scaled_kkt_rows(dm.struct, nat.ptr(xd), nat.ptr(td), nat.ptr(pd),
+                                        nat.ptr(yd), float(xi), nat.ptr(out), nat.ptr(scratch),
+                                        _cur_stream()), "mq_scaled_kkt_rows")
+    cs = torch.zeros(dm.m, dtype=torch.float64, device=dm.device)
+    nat.check(dm.lib.mq_colsum(dm.struct, nat.ptr(xd), nat.ptr(cs), _cur_stream()), "mq_colsum")
+    bud, comp, viol, link = (float(v) for v in out.cpu().numpy())
+    col = float(((cs - 1.0) ** 2).sum().item())
+    return float(math.sqrt(bud + comp + viol + col + link))  # kkt.py:106-111 order
+
+
+def scaled_kkt_residual_compact(inst, x, p, xi=1.0):
+    """Scaled KKT residual of a compact state via t = u.x, y = w/t
+    (kkt.py:114-121)."""
+    import numpy as np
+
+    ux = inst.utilities.row_sums(inst.utilities.values * np.asarray(x, dtype=np.float64))
+    if np.any(ux <= 0):
+        raise ValueError("compact state has a zero-utility buyer")
+    return scaled_kkt_residual(inst, x, ux, p, inst.budgets / ux, xi)
+
+
+def smoothed_gap(inst, z, center, xi=1.0, sections=32, subtol=1e-12):
+    """Smoothed duality gap of z = (x, p) centered at (x_c, p_c)
+    (kkt.py:134-168).  The price maximization is the exact quadratic; the
+    allocation minimization is the exact per-buyer prox with step 1/xi, on the
+    device (the reference's k-section with `sections`/`subtol` finds the same
+    root to its tolerance; both arguments are accepted for compatibility)."""
+    import math
+
+    import numpy as np
+    import torch
+
+    from . import _native as nat
+    from .device import DeviceMarket
+    from .engine import _cur_stream
+
+    if xi <= 0:
+        raise ValueError("xi must be positive")
+    x, p = (np.asarray(a, dtype=np.float64) for a in z)
+    x_c, p_c = (np.asarray(a, dtype=np.float64) for a in center)
+    f_x = eg_objective(inst, x)
+    if not np.isfinite(f_x):
+        return math.inf
+    dm = DeviceMarket.from_instance(inst)
+    xd, pd, xcd = (_dev(a, dm) for a in (x, p, x_c))
+    cs = torch.zeros(dm.m, dtype=torch.float64, device=dm.device)
+    nat.check(dm.lib.mq_colsum(dm.struct, nat.ptr(xd), nat.ptr(cs), _cur_stream()), "mq_colsum")
+    r = cs.cpu().numpy() - 1.0
+    best_price_part = f_x + float(np.dot(p_c, r)) + float(np.dot(r, r)) / (2.0 * xi)
+    cbuf = torch.zeros(max(1, dm.nnz), dtype=torch.float64, device=dm.device)
+    out = torch.zeros(1, dtype=torch.float64, device=dm.device)
+    faults = torch.zeros(1, dtype=torch.int64, device=dm.device)
+    scratch = torch.zeros(int(dm.lib.mq_scratch_doubles()), dtype=torch.float64,
+                          device=dm.device)
+    nat.check(dm.lib.mq_smoothed_gap_rows(dm.struct, nat.ptr(xcd), nat.ptr(pd), float(xi),
+                                          nat.ptr(cbuf), nat.ptr(out), nat.ptr(scratch),
+                                          nat.ptr(faults), _cur_stream()), "mq_smoothed_gap_rows")
+    if int(faults.item()):
+        from .errors import SubproblemError
+
+        raise SubproblemError("smoothed gap: a row prox did not settle")
+    return best_price_part + float(np.sum(p)) - float(out.item())
