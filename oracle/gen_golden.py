@@ -14,6 +14,8 @@ Fixtures (all float64 stored exactly):
   solve_*.npz    instance -> run_solve(...) report               (full solves)
   pdhg_*.npz     instance -> run_solve(..., "pdhg") report       (lifted PDHG solves)
   theory.npz     random states -> kkt.scaled_kkt_residual(_compact), kkt.smoothed_gap
+  fileio/        instance files written by fileio.save + malformed files with the
+                 reference reader's errors (errors.json)
   resid.npz      random states -> kkt.residuals_compact           (residual formulas)
   exchange.npz   generate_exchange -> solve_exchange trace       (Arrow-Debreu)
   gen.json       generator fingerprints (instance_fingerprint)   (generator parity)
@@ -291,6 +293,53 @@ def theory_case():
     save("theory.npz", **out)
 
 
+FILEIO_BAD = {
+    "bad_header.mtx": "%%MatrixMarket matrix array real general\n2 2 1\n1 1 0.5\n",
+    "bad_size.mtx": "%%MatrixMarket matrix coordinate real general\n2 2\n1 1 0.5\n",
+    "bad_index.mtx": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 0.5\n3 1 0.5\n",
+    "bad_neg.mtx": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 0.5\n2 1 -0.5\n",
+    "bad_count.mtx": "%%MatrixMarket matrix coordinate real general\n% c\n2 2 3\n1 1 0.5\n2 2 0.5\n",
+    "bad_malformed.mtx": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 0.5\n2 x 0.5\n",
+    "bad_float_index.mtx": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 0.5\n2.0 1 0.5\n",
+    "bad_many.mtx": "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 0.5\n2 2 0.5\n",
+    "bad_cols.csv": "2,2,2\n0,0,0.5\n1,0\n",
+    "bad_hdr.csv": "2,2\n0,0,0.5\n",
+    "bad_idx.csv": "2,2,2\n0,0,0.5\n0,2,0.5\n",
+    "ok_comments.mtx": ("%%MatrixMarket matrix coordinate real general\n% hi\n2 2 2\n1 1 0.5\n"
+                        "% mid\n\n2 2 0.25\n"),
+}
+
+
+def fileio_case():
+    """Files the reference's fileio.save writes, and its reader's verdicts on
+    malformed files (message, line)."""
+    from market_eq import fileio as rf
+
+    out = os.path.join(OUT, "fileio")
+    os.makedirs(out, exist_ok=True)
+    inst = me.generate_fisher(me.GeneratorConfig(n=30, m=12, sparsity_u=0.3, seed=4))
+    ex = me.generate_exchange(me.GeneratorConfig(n=10, m=8, sparsity_u=0.4, seed=2))
+    rf.save(inst, os.path.join(out, "fisher"), "mtx")
+    rf.save(inst, os.path.join(out, "fisher"), "csv")
+    rf.save(ex, os.path.join(out, "exch"), "mtx")
+    msgs = {}
+    for name, text in FILEIO_BAD.items():
+        path = os.path.join(out, name)
+        with open(path, "w") as fh:
+            fh.write(text)
+        reader = rf.read_matrix_market if name.endswith(".mtx") else rf.read_csv_triplets
+        try:
+            M = reader(path)
+            msgs[name] = {"ok": True, "values": M.values.tolist(), "col": M.col_indices.tolist(),
+                          "rows": M.row_offsets.tolist()}
+        except Exception as e:  # noqa: BLE001 - record the reference's verdict
+            msgs[name] = {"ok": False, "type": type(e).__name__, "line": getattr(e, "line", None),
+                          "msg": str(e).replace(out + "/", "")}
+    with open(os.path.join(out, "errors.json"), "w") as fh:
+        json.dump(msgs, fh, indent=1)
+    print(f"  fileio: {len(msgs)} reader cases")
+
+
 def c1_instance():
     """BASELINE config 1: dense 1000x500, U~U(0,1) (default_rng(0)), w=1."""
     U = np.random.default_rng(0).random((1000, 500))
@@ -441,7 +490,7 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     orc.set_threads(os.cpu_count())
     steps = {"chunk": chunk_cases, "rowroot": rowroot_cases, "solve": lambda: solve_cases(a.big),
-             "pdhg": pdhg_cases, "theory": theory_case,
+             "pdhg": pdhg_cases, "theory": theory_case, "fileio": fileio_case,
              "bigsolve": big_solve_cases,
              "resid": resid_cases, "exchange": exchange_case,
              "gen": lambda: gen_fingerprints(a.big), "c2": c2_lockstep}
