@@ -138,3 +138,33 @@ def smoothed_gap(inst, z, center, xi=1.0, sections=32, subtol=1e-12):
 
         raise SubproblemError("smoothed gap: a row prox did not settle")
     return best_price_part + float(np.sum(p)) - float(out.item())
+
+
+def residuals_lifted(inst, x, t, p, y):
+    """Relative KKT residuals of a lifted state (x, t, p, y) on `inst`
+    (kkt.py:29-76), on the device.  Raises ValueError unless every t > 0."""
+    import numpy as np
+    import torch
+
+    from . import _native as nat
+    from .device import DeviceMarket
+    from .engine import _cur_stream
+    from .lifted import LiftedEngine
+
+    dm = DeviceMarket.from_instance(inst)
+    xd, td, pd, yd = (_dev(a, dm) for a in (x, t, p, y))
+    ones = torch.ones(dm.n, dtype=torch.float64, device=dm.device)  # (t, y) given as-is
+    out = torch.zeros(16, dtype=torch.float64, device=dm.device)
+    colbest = torch.zeros(dm.m, dtype=torch.float64, device=dm.device)
+    scratch = torch.zeros(int(dm.lib.mq_scratch_doubles()), dtype=torch.float64,
+                          device=dm.device)
+    nat.check(dm.lib.mq_pdhg_resid_rows(dm.struct, nat.ptr(ones), nat.ptr(xd), nat.ptr(td),
+                                        nat.ptr(yd), nat.ptr(pd), 0, nat.ptr(colbest),
+                                        nat.ptr(out[0:10]), nat.ptr(scratch), _cur_stream()),
+              "mq_pdhg_resid_rows")
+    cs = torch.zeros(dm.m, dtype=torch.float64, device=dm.device)
+    nat.check(dm.lib.mq_colsum(dm.struct, nat.ptr(xd), nat.ptr(cs), _cur_stream()), "mq_colsum")
+    nat.check(dm.lib.mq_resid_cols(dm.m, nat.ptr(cs), nat.ptr(pd), nat.ptr(colbest),
+                                   nat.ptr(out[10:16]), nat.ptr(scratch), _cur_stream()),
+              "mq_resid_cols")
+    return LiftedEngine._assemble(out.cpu().numpy())
