@@ -696,17 +696,36 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
     const double tau = st.steps[0];
     int64_t my_sweeps = 0;
     int my_faults = 0;
+    // c = x - tau p[col] is kept in the row's x slots across the sweeps (one
+    // price gather per entry instead of one per sweep); every thread touches
+    // the same entries in every pass
+    double *__restrict__ cx = st.x;
+    constexpr int LB = 4;
     for (int64_t r = blockIdx.x; r < mk.nlong; r += gridDim.x) {
         const int64_t i = mk.long_rows[r];
         const int64_t a = mk.row_ptr[i], b = mk.row_ptr[i + 1];
         const double tw = tau * mk.w[i];
         double s0 = 0.0, A = 0.0, B = 0.0;
-        for (int64_t t = a + threadIdx.x; t < b; t += blockDim.x) {
-            const double ue = mk.u[t], xe = st.x[t];
-            const double ce = xe - tau * st.p[mk.col[t]];
-            s0 += ue * xe;
-            A += ue * ce;
-            B += ue * ue;
+        for (int64_t t0 = a + threadIdx.x; t0 < b; t0 += LB * blockDim.x) {
+            double xv[LB], pv[LB];
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {  // all loads of the batch before its stores
+                const int64_t t = t0 + q * blockDim.x;
+                xv[q] = t < b ? cx[t] : 0.0;
+                pv[q] = t < b ? __ldg(st.p + mk.col[t]) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                const int64_t t = t0 + q * blockDim.x;
+                if (t < b) {
+                    const double ue = mk.u[t], ce = xv[q] - tau * pv[q];
+                    if (x_prev_out) x_prev_out[t] = xv[q];
+                    cx[t] = ce;
+                    s0 += ue * xv[q];
+                    A += ue * ce;
+                    B += ue * ue;
+                }
+            }
         }
         block_sum3(s0, A, B, sm);
         double s = active_root(A, B, tw);
@@ -719,7 +738,7 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
             cnt = 0.0;
             for (int64_t t = a + threadIdx.x; t < b; t += blockDim.x) {
                 const double ue = mk.u[t];
-                const double ce = st.x[t] - tau * st.p[mk.col[t]];
+                const double ce = cx[t];
                 if (fma(ce, q, tw * ue) > 0.0) {
                     As += ue * ce;
                     Bs += ue * ue;
@@ -759,12 +778,18 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
             st.srow[i] = s;
         }
         const double inv_s = 1.0 / s;
-        __syncthreads();  // every sweep has read x before it is overwritten
-        for (int64_t t = a + threadIdx.x; t < b; t += blockDim.x) {
-            const double xe = st.x[t];
-            if (x_prev_out) x_prev_out[t] = xe;
-            const double xn = fmax(xe - tau * st.p[mk.col[t]] + tw * mk.u[t] * inv_s, 0.0);
-            put_x(mk, st, t, mk.col[t], xn, true);
+        for (int64_t t0 = a + threadIdx.x; t0 < b; t0 += LB * blockDim.x) {
+            double cv[LB];
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                const int64_t t = t0 + q * blockDim.x;
+                cv[q] = t < b ? cx[t] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                const int64_t t = t0 + q * blockDim.x;
+                if (t < b) put_x(mk, st, t, mk.col[t], fmax(cv[q] + tw * mk.u[t] * inv_s, 0.0), true);
+            }
         }
         __syncthreads();
     }
