@@ -53,7 +53,7 @@ typedef struct mq_market {
        and MQ_TILE_ROWS rows, no row longer than MQ_LONG_ROW (32-byte aligned) */
     const int64_t *tiles;
     int64_t ntiles;
-    const int32_t *long_rows; /* rows longer than MQ_LONG_ROW                   */
+    const int32_t *long_rows; /* rows longer than MQ_LONG_ROW, longest first    */
     int64_t nlong;
     /* tile-blocked transpose schedule of the deterministic fp64 column sums
        (mq_colsum: residual checks, restarts): the tiles are grouped in blocks
@@ -85,7 +85,8 @@ typedef struct mq_state {
     double *cs;       /* [m]   colsum(x^k)                                     */
     double *cs_prev;  /* [m]   colsum(x^{k-1})                                 */
     double *csbar;    /* [m]   colsum(xbar)                                    */
-    int32_t *blk_done;/* [1] the primal kernel's dynamic tile counter         */
+    int32_t *blk_done;/* [2] the primal kernels' dynamic work counters (tiles,
+                         long rows)                                            */
     const double *steps; /* [2] tau, sigma (device-resident: one graph serves
                             every step size)                                   */
     int64_t *navg;    /* [1]  inner iterations since the last restart          */

@@ -59,6 +59,9 @@
 #ifndef MQ_LB
 #define MQ_LB 8  // entries per lane batched ahead of the stores (longer rows)
 #endif
+#ifndef MQ_LONG_THREADS
+#define MQ_LONG_THREADS 256  // threads per CTA of the long-row kernel (one row per CTA)
+#endif
 
 namespace mq {
 
@@ -690,7 +693,7 @@ __device__ __forceinline__ void block_sum3(double &a, double &b, double &c, doub
     c = group_sum<32>(rc);
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(MQ_LONG_THREADS)
 primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
     __shared__ double sm[96];
     const double tau = st.steps[0];
@@ -701,7 +704,14 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
     // the same entries in every pass
     double *__restrict__ cx = st.x;
     constexpr int LB = 4;
-    for (int64_t r = blockIdx.x; r < mk.nlong; r += gridDim.x) {
+    __shared__ int64_t claimed;
+    // rows (longest first) are claimed one at a time from a global counter
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) claimed = atomicAdd(st.blk_done + 1, 1);
+        __syncthreads();
+        const int64_t r = claimed;
+        if (r >= mk.nlong) break;
         const int64_t i = mk.long_rows[r];
         const int64_t a = mk.row_ptr[i], b = mk.row_ptr[i + 1];
         const double tw = tau * mk.w[i];
@@ -894,8 +904,9 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
                                                                    mk->ntiles, st->blk_done);
     }
     if (mk->nlong > 0) {
+        cudaMemsetAsync(st->blk_done + 1, 0, sizeof(int32_t), s);  // long-row counter
         const int grid = grid_for(mk->nlong, 1, sm_count() * 8);
-        primal_long_kernel<<<grid, 256, 0, s>>>(*mk, *st, it, xprev);
+        primal_long_kernel<<<grid, MQ_LONG_THREADS, 0, s>>>(*mk, *st, it, xprev);
     }
     return check_launch("mq_primal_step");
 }

@@ -199,6 +199,11 @@ class DeviceMarket:
             etile = int(self.lib.mq_tile_entries())
             tiles2, self.long_rows = build_tiles(self.row_ptr, etile,
                                                  min(nat.LONG_ROW, etile // 2))
+            if self.long_rows.numel() > 1:  # longest first: the CTAs claim them in order
+                lr = self.long_rows.to(torch.int64)
+                order = torch.argsort(self.row_ptr[lr + 1] - self.row_ptr[lr], descending=True,
+                                      stable=True)
+                self.long_rows = self.long_rows[order].contiguous()
             # (r0, r1, e0, e1) per tile: the producer warp needs no dependent loads
             self.tiles = torch.cat([tiles2, self.row_ptr[tiles2]], 1).contiguous()
             self.prim_grid = int(min(max(1, self.tiles.shape[0]), sm_count(dev)))
