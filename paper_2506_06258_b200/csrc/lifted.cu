@@ -155,7 +155,8 @@ resid_lifted_rows_kernel(const mq_market mk, const double *__restrict__ scales,
         for (int64_t e = mk.row_ptr[i] + lane; e < mk.row_ptr[i + 1]; e += 32) {
             const int j = mk.col[e];
             const double uy = U[e] * yo;
-            atomicMax(colkey + j, okey(uy));
+            const unsigned long long kk = okey(uy);
+            if (kk > __ldcg(colkey + j)) atomicMax(colkey + j, kk);  // skip covered values
             const double es = fmax(p[j] - uy, 0.0);
             const double xv = x[e];
             gmax = fmax(gmax, xv * es);

@@ -37,30 +37,41 @@ __global__ void sum_slots_kernel(const double *__restrict__ partials, int nblock
     }
 }
 
+// One G-lane group per buyer (32/G buyers per warp in flight: the row pass is
+// latency-bound, so more rows per warp hide more of it).  The row loop is
+// warp-uniform; only the entry loops diverge.
+template <int G>
 __global__ void __launch_bounds__(256)
 resid_rows_kernel(const mq_market mk, const double *__restrict__ x, const double *__restrict__ p,
                   int use_norm, double *__restrict__ colbest, double *__restrict__ t_out,
                   double *__restrict__ y_out, double *__restrict__ scratch) {
     const double *__restrict__ U = use_norm ? mk.u : mk.u_orig;
-    const int lane = threadIdx.x & 31;
+    constexpr int RPW = 32 / G;  // rows per warp
+    const int lane = threadIdx.x & (G - 1);
+    const int gsub = (threadIdx.x & 31) / G;
     const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     double *misc = scratch + kMisc;
     double ymax = 0.0, gmax = 0.0, xmax = 0.0, emax = 0.0, obj = 0.0, nbad = 0.0;
-    for (int64_t i = warp_id; i < mk.n; i += nwarps) {
-        const int64_t a = mk.row_ptr[i], b = mk.row_ptr[i + 1];
-        double tp = 0.0;
-        for (int64_t t = a + lane; t < b; t += 32) tp += U[t] * x[t];
-        const double t_i = group_sum<32>(tp);
-        if (!(t_i > 0.0)) {
-            if (lane == 0) {
-                nbad += 1.0;
-                atomicMin((unsigned long long *)(misc + 4), (unsigned long long)(mk.row_begin + i));
-                if (t_out) t_out[i] = t_i;
-                if (y_out) y_out[i] = 0.0;
-            }
-            continue;
+    for (int64_t base = warp_id * RPW; base < mk.n; base += nwarps * RPW) {
+        const int64_t i = base + gsub;
+        const bool has = i < mk.n;
+        int64_t a = 0, b = 0;
+        if (has) {
+            a = mk.row_ptr[i];
+            b = mk.row_ptr[i + 1];
         }
+        double tp = 0.0;
+        for (int64_t t = a + lane; t < b; t += G) tp += U[t] * x[t];
+        const double t_i = group_sum<G>(tp);
+        const bool ok = has && t_i > 0.0;
+        if (has && !ok && lane == 0) {
+            nbad += 1.0;
+            atomicMin((unsigned long long *)(misc + 4), (unsigned long long)(mk.row_begin + i));
+            if (t_out) t_out[i] = t_i;
+            if (y_out) y_out[i] = 0.0;
+        }
+        if (!ok) continue;  // no collectives below
         const double y = mk.w[i] / t_i;
         if (lane == 0) {
             obj += mk.w[i] * log(t_i);
@@ -68,10 +79,12 @@ resid_rows_kernel(const mq_market mk, const double *__restrict__ x, const double
             if (t_out) t_out[i] = t_i;
             if (y_out) y_out[i] = y;
         }
-        for (int64_t t = a + lane; t < b; t += 32) {
+        for (int64_t t = a + lane; t < b; t += G) {
             const int32_t j = mk.col[t];
             const double uy = U[t] * y;
-            atomic_max_nonneg(colbest + j, uy);
+            // skip the atomic when the column's current maximum already covers
+            // uy (a stale read only under-estimates it: still order-free)
+            if (uy > __ldcg(colbest + j)) atomic_max_nonneg(colbest + j, uy);
             const double es = fmax(p[j] - uy, 0.0);
             const double xv = x[t];
             gmax = fmax(gmax, xv * es);
@@ -79,10 +92,11 @@ resid_rows_kernel(const mq_market mk, const double *__restrict__ x, const double
             emax = fmax(emax, es);
         }
     }
+    ymax = group_max<32>(ymax);  // each group's lane 0 holds its rows' maximum
     gmax = group_max<32>(gmax);
     xmax = group_max<32>(xmax);
     emax = group_max<32>(emax);
-    if (lane == 0) {
+    if ((threadIdx.x & 31) == 0) {
         atomic_max_nonneg(misc + 0, ymax);
         atomic_max_nonneg(misc + 1, gmax);
         atomic_max_nonneg(misc + 2, xmax);
@@ -237,7 +251,7 @@ int mq_resid_rows(const mq_market *mk, const double *x, const double *p, int use
     const int grid = grid_for(mk->n, 8, MQ_MAX_BLOCKS);
     cudaMemsetAsync(scratch + kMisc, 0, 4 * sizeof(double), s);
     cudaMemsetAsync(scratch + kMisc + 4, 0xff, sizeof(double), s);
-    resid_rows_kernel<<<grid, 256, 0, s>>>(*mk, x, p, use_norm, colbest, t_out, y_out, scratch);
+    resid_rows_kernel<8><<<grid, 256, 0, s>>>(*mk, x, p, use_norm, colbest, t_out, y_out, scratch);
     sum_slots_kernel<<<1, 64, 0, s>>>(scratch, grid, 2, scratch + kMisc + 16);
     resid_rows_finish<<<1, 1, 0, s>>>(scratch, scratch + kMisc + 16, row_out);
     return check_launch("mq_resid_rows");
