@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define MQ_ABI_VERSION 5
+#define MQ_ABI_VERSION 6
 #define MQ_TILE_ENTRIES 2560 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
@@ -182,9 +182,11 @@ int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream);
  * [2] max |x|, [3] max (p-uy)_+, [4] first row with t <= 0 (as double, or -1),
  * [5] sum_i w_i log t_i (fixed order), [6] rows with t <= 0, [7] unused.
  * t_out / y_out (may be NULL) receive t and y per local row.
- * colbest must be zero-initialised by the caller (values are positive). */
+ * colbest must be zero-initialised by the caller (values are positive).
+ * work: 2m doubles of workspace (p and the running column maxima interleaved,
+ * one random access per entry), or NULL for a stream-ordered temporary. */
 int mq_resid_rows(const mq_market *mk, const double *x, const double *p, int use_norm,
-                  double *colbest, double *t_out, double *y_out, double *row_out,
+                  double *colbest, double *work, double *t_out, double *y_out, double *row_out,
                   double *scratch, void *stream);
 /* Column pass (replicated data): col_out[6] (device):
  * [0] max |cs - 1|, [1] max |cs|, [2] max (colbest - p)_+, [3] max (p - colbest)

@@ -17,7 +17,7 @@ TILE_ENTRIES = 2560   # MQ_TILE_ENTRIES
 LONG_ROW = 1024       # MQ_LONG_ROW
 TILE_ROWS = 256       # MQ_TILE_ROWS
 PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 _lock = threading.Lock()
 _lib = None
@@ -75,7 +75,7 @@ _SIGS = {
     "mq_chunk_end": (CINT, [PS, CINT, P]),
     "mq_fast_chunk": (CINT, [PM, PS, CINT, P]),
     "mq_colsum": (CINT, [PM, P, P, P]),
-    "mq_resid_rows": (CINT, [PM, P, P, CINT, P, P, P, P, P, P]),
+    "mq_resid_rows": (CINT, [PM, P, P, CINT, P, P, P, P, P, P, P]),
     "mq_resid_cols": (CINT, [I64, P, P, P, P, P, P]),
     "mq_restart_moves": (CINT, [PM, P, P, P, P, P, P, P, P, P]),
     "mq_spmv": (CINT, [I64, P, P, P, P, P, P]),

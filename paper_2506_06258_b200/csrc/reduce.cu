@@ -40,11 +40,13 @@ __global__ void sum_slots_kernel(const double *__restrict__ partials, int nblock
 // One G-lane group per buyer (32/G buyers per warp in flight: the row pass is
 // latency-bound, so more rows per warp hide more of it).  The row loop is
 // warp-uniform; only the entry loops diverge.
+// pc[2j] = p_j and pc[2j+1] = the running column maximum share one 16-byte
+// slot, so the entry pass makes one random access per entry for both
 template <int G>
 __global__ void __launch_bounds__(256)
-resid_rows_kernel(const mq_market mk, const double *__restrict__ x, const double *__restrict__ p,
-                  int use_norm, double *__restrict__ colbest, double *__restrict__ t_out,
-                  double *__restrict__ y_out, double *__restrict__ scratch) {
+resid_rows_kernel(const mq_market mk, const double *__restrict__ x, double2 *__restrict__ pc,
+                  int use_norm, double *__restrict__ t_out, double *__restrict__ y_out,
+                  double *__restrict__ scratch) {
     const double *__restrict__ U = use_norm ? mk.u : mk.u_orig;
     constexpr int RPW = 32 / G;  // rows per warp
     const int lane = threadIdx.x & (G - 1);
@@ -82,10 +84,11 @@ resid_rows_kernel(const mq_market mk, const double *__restrict__ x, const double
         for (int64_t t = a + lane; t < b; t += G) {
             const int32_t j = mk.col[t];
             const double uy = U[t] * y;
+            const double2 pcj = __ldcg(pc + j);
             // skip the atomic when the column's current maximum already covers
             // uy (a stale read only under-estimates it: still order-free)
-            if (uy > __ldcg(colbest + j)) atomic_max_nonneg(colbest + j, uy);
-            const double es = fmax(p[j] - uy, 0.0);
+            if (uy > pcj.y) atomic_max_nonneg(reinterpret_cast<double *>(pc + j) + 1, uy);
+            const double es = fmax(pcj.x - uy, 0.0);
             const double xv = x[t];
             gmax = fmax(gmax, xv * es);
             xmax = fmax(xmax, fabs(xv));
@@ -109,6 +112,18 @@ resid_rows_kernel(const mq_market mk, const double *__restrict__ x, const double
         scratch[kSlotObj * MQ_MAX_BLOCKS + blockIdx.x] = ob;
         scratch[kSlotBad * MQ_MAX_BLOCKS + blockIdx.x] = nb;
     }
+}
+
+__global__ void pc_init_kernel(int64_t m, const double *__restrict__ p, double2 *__restrict__ pc) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x)
+        pc[j] = make_double2(p[j], 0.0);
+}
+__global__ void pc_out_kernel(int64_t m, const double2 *__restrict__ pc,
+                              double *__restrict__ colbest) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x)
+        colbest[j] = fmax(colbest[j], pc[j].y);
 }
 
 __global__ void resid_rows_finish(const double *__restrict__ scratch, const double *__restrict__ sums,
@@ -245,13 +260,23 @@ extern "C" {
 int64_t mq_scratch_doubles(void) { return MQ_SCRATCH_DOUBLES; }
 
 int mq_resid_rows(const mq_market *mk, const double *x, const double *p, int use_norm,
-                  double *colbest, double *t_out, double *y_out, double *row_out, double *scratch,
-                  void *stream) {
+                  double *colbest, double *work, double *t_out, double *y_out, double *row_out,
+                  double *scratch, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     const int grid = grid_for(mk->n, 8, MQ_MAX_BLOCKS);
     cudaMemsetAsync(scratch + kMisc, 0, 4 * sizeof(double), s);
     cudaMemsetAsync(scratch + kMisc + 4, 0xff, sizeof(double), s);
-    resid_rows_kernel<8><<<grid, 256, 0, s>>>(*mk, x, p, use_norm, colbest, t_out, y_out, scratch);
+    double2 *pc = reinterpret_cast<double2 *>(work);
+    if (!pc) {  // no caller workspace: a stream-ordered temporary
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&pc),
+                                        (size_t)(mk->m > 0 ? mk->m : 1) * sizeof(double2), s);
+        if (e != cudaSuccess) return set_error(e, "mq_resid_rows: workspace");
+    }
+    const int gm = grid_for(mk->m, 256, MQ_MAX_BLOCKS);
+    pc_init_kernel<<<gm, 256, 0, s>>>(mk->m, p, pc);
+    resid_rows_kernel<8><<<grid, 256, 0, s>>>(*mk, x, pc, use_norm, t_out, y_out, scratch);
+    pc_out_kernel<<<gm, 256, 0, s>>>(mk->m, pc, colbest);
+    if (!work) cudaFreeAsync(pc, s);
     sum_slots_kernel<<<1, 64, 0, s>>>(scratch, grid, 2, scratch + kMisc + 16);
     resid_rows_finish<<<1, 1, 0, s>>>(scratch, scratch + kMisc + 16, row_out);
     return check_launch("mq_resid_rows");

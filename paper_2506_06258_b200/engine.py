@@ -145,9 +145,11 @@ class NativeOps:
                     "mq_avg_materialize")
 
     def resid_rows(self, x, p, use_norm, colbest, t_out, out, scratch):
+        work = self.eng.resid_work
         self._c(self.lib.mq_resid_rows(self.dm.struct, nat.ptr(x), nat.ptr(p), int(use_norm),
-                                       nat.ptr(colbest), nat.ptr(t_out), None, nat.ptr(out),
-                                       nat.ptr(scratch), _cur_stream()), "mq_resid_rows")
+                                       nat.ptr(colbest), nat.ptr(work), nat.ptr(t_out), None,
+                                       nat.ptr(out), nat.ptr(scratch), _cur_stream()),
+                "mq_resid_rows")
 
     def resid_cols(self, cs, p, colbest, out, scratch):
         self._c(self.lib.mq_resid_cols(self.dm.m, nat.ptr(cs), nat.ptr(p), nat.ptr(colbest),
@@ -229,6 +231,7 @@ class PdhcgEngine:
         self.csbar = torch.zeros(m, **f64)
         self.cs0 = torch.zeros(m, **f64)
         self.colbest = torch.zeros(2, m, **f64)
+        self.resid_work = torch.zeros(2 * max(1, m), **f64)  # (p, column max) interleaved
         self.steps = torch.zeros(2, **f64)
         self.navg_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         self.faults = torch.zeros(1, dtype=torch.int64, device=dev)

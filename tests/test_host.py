@@ -24,7 +24,7 @@ def test_native_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(lib, name)
-    assert lib.mq_abi_version() == 5
+    assert lib.mq_abi_version() == 6
     assert lib.mq_scratch_doubles() > 0
 
 
@@ -166,7 +166,7 @@ def test_abi_marshaling_without_device():
         "mq_chunk_end": (st, 1, None),
         "mq_fast_chunk": (mk, st, 1, None),
         "mq_colsum": (mk, None, None, None),
-        "mq_resid_rows": (mk, None, None, 0, None, None, None, None, None, None),
+        "mq_resid_rows": (mk, None, None, 0, None, None, None, None, None, None, None),
         "mq_resid_cols": (0, None, None, None, None, None, None),
         "mq_restart_moves": (mk, None, None, None, None, None, None, None, None, None),
         "mq_spmv": (0, None, None, None, None, None, None),
