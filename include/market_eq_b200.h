@@ -32,10 +32,12 @@
 extern "C" {
 #endif
 
-#define MQ_ABI_VERSION 6
+#define MQ_ABI_VERSION 7
 #define MQ_TILE_ENTRIES 2560 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
+#define MQ_REG_ROW 128        /* tile rows longer than this (medium rows) are
+                                 solved by the warp-per-row path          */
 
 /* Read-only market description (device pointers, borrowed).  Arrays marked
  * [pad] must have 16 readable bytes past their last element (TMA bulk copies
@@ -55,6 +57,11 @@ typedef struct mq_market {
     int64_t ntiles;
     const int32_t *long_rows; /* rows longer than MQ_LONG_ROW, longest first    */
     int64_t nlong;
+    /* medium rows: tile rows longer than MQ_REG_ROW, longest first; the tile
+       kernel skips them (their entries are still staged) and the warp-per-row
+       kernel solves them, so no tile stage waits on one slow row             */
+    const int32_t *med_rows;
+    int64_t nmed;
     /* tile-blocked transpose schedule of the deterministic fp64 column sums
        (mq_colsum: residual checks, restarts): the tiles are grouped in blocks
        of tiles_per_block consecutive tiles; bperm lists, block by block and
@@ -85,8 +92,8 @@ typedef struct mq_state {
     double *cs;       /* [m]   colsum(x^k)                                     */
     double *cs_prev;  /* [m]   colsum(x^{k-1})                                 */
     double *csbar;    /* [m]   colsum(xbar)                                    */
-    int32_t *blk_done;/* [2] the primal kernels' dynamic work counters (tiles,
-                         long rows)                                            */
+    int32_t *blk_done;/* [3] the primal kernels' dynamic work counters (tiles,
+                         long rows, medium rows)                               */
     const double *steps; /* [2] tau, sigma (device-resident: one graph serves
                             every step size)                                   */
     int64_t *navg;    /* [1]  inner iterations since the last restart          */
@@ -274,6 +281,10 @@ int mq_gen_fill(int64_t row0, int64_t nrows, int64_t m, int q_mode, double q, do
 /* Entries per primal tile this build was compiled for (tiles must not exceed
  * it; MQ_TILE_ENTRIES by default). */
 int mq_tile_entries(void);
+
+/* Longest tile row the tile kernel solves itself (MQ_REG_ROW); longer tile
+ * rows go in mq_market.med_rows. */
+int mq_reg_row(void);
 
 /* How this build computes the price step's column sums: 5 = fixed-point
  * atomics on the nonzero entries (the only mode of this build; the earlier

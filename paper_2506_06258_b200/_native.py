@@ -15,9 +15,10 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MQ_LIB") or os.path.join(_PKG, "libmarket_eq_b200.so")
 TILE_ENTRIES = 2560   # MQ_TILE_ENTRIES
 LONG_ROW = 1024       # MQ_LONG_ROW
+REG_ROW = 128         # MQ_REG_ROW
 TILE_ROWS = 256       # MQ_TILE_ROWS
 PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 _lock = threading.Lock()
 _lib = None
@@ -40,6 +41,7 @@ class MqMarket(ctypes.Structure):
     _fields_ = [("n", I64), ("m", I64), ("nnz", I64),
                 ("row_ptr", P), ("col", P), ("u", P), ("u_orig", P), ("w", P),
                 ("tiles", P), ("ntiles", I64), ("long_rows", P), ("nlong", I64),
+                ("med_rows", P), ("nmed", I64),
                 ("bperm", P), ("bptr", P), ("nblk", I64), ("tiles_per_block", I64),
                 ("prim_grid", ctypes.c_int32), ("row_begin", I64),
                 ("cs_scale", ctypes.c_double), ("cs_xmax", ctypes.c_double)]
@@ -85,6 +87,7 @@ _SIGS = {
                            P]),
     "mq_scratch_doubles": (I64, []),
     "mq_tile_entries": (CINT, []),
+    "mq_reg_row": (CINT, []),
     "mq_colsum_mode": (CINT, []),
     "mq_last_error": (ctypes.c_char_p, []),
     "mq_abi_version": (CINT, []),

@@ -60,7 +60,10 @@
 #define MQ_LB 8  // entries per lane batched ahead of the stores (longer rows)
 #endif
 #ifndef MQ_LONG_THREADS
-#define MQ_LONG_THREADS 256  // threads per CTA of the long-row kernel (one row per CTA)
+#define MQ_LONG_THREADS 512  // threads per CTA of the long-row kernel (one row per CTA)
+#endif
+#ifndef MQ_LONG_CAP
+#define MQ_LONG_CAP 5120  // entries of a long row kept in shared memory (107.5 KB, 2 CTAs/SM)
 #endif
 
 namespace mq {
@@ -591,10 +594,15 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 MQ_TA(6, tq1, tq2);
                 MQ_TA(7, tq2, tq3);
             } else {
-                // ---- longer rows: c is kept in the row's x slots across the
-                // sweeps; batches of MQ_LB entries per lane keep all loads of a
-                // batch in flight before its c values are stored over x (the
-                // stores could alias the next loads, which would serialize them)
+                // ---- a pair with a medium row (longer than the registers
+                // hold): primal_med_kernel solves that row (one slow row here
+                // would hold the stage); a short partner row is solved here
+                // with c kept in its x slots across the sweeps; batches of
+                // MQ_LB entries per lane keep all loads of a batch in flight
+                // before its c values are stored over x (the stores could
+                // alias the next loads, which would serialize them)
+                const bool med = b - a > MQ_REG_PER * G;
+                if (med) b = a;
                 double *sc = st.x + e0;
                 double s0p = 0.0, ap = 0.0, bp = 0.0;
                 for (int t0 = a + lane; t0 < b; t0 += MQ_LB * G) {
@@ -625,7 +633,7 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 const double B = group_sum<G>(bp);
                 const double sr =
                     row_root_exact<G>(su, sc, a, b, lane, tw, s0, A, B, has, &nsw, &ok);
-                if (has && lane == 0) st.srow[r0 + r] = sr;
+                if (has && !med && lane == 0) st.srow[r0 + r] = sr;
                 const double inv_s = 1.0 / sr;
                 for (int t0 = a + lane; t0 < b; t0 += MQ_LB * G) {
                     double cv[MQ_LB];
@@ -693,62 +701,106 @@ __device__ __forceinline__ void block_sum3(double &a, double &b, double &c, doub
     c = group_sum<32>(rc);
 }
 
-__global__ void __launch_bounds__(MQ_LONG_THREADS)
+// One CTA per long row (rows claimed longest first from a global counter).
+// The row's first MQ_LONG_CAP entries stay in shared memory across the
+// sweeps (u, c = x - tau p[col], col, was-nonzero flag: 21 bytes per entry),
+// so a long row streams its u / col / flags once and its x only where
+// flagged, like a tile row; entries past the cap keep c in their x slots.
+// Entry k of the row belongs to thread k mod MQ_LONG_THREADS in every pass,
+// so each thread re-reads only what it wrote.
+template <int T, int CAP>
+struct LongSmem {
+    static constexpr int kU = 0, kC = CAP * 8, kJ = 2 * CAP * 8, kF = kJ + CAP * 4;
+    static constexpr int kBytes = kF + CAP;
+};
+
+template <int T, int CAP>
+__global__ void __launch_bounds__(T, 2048 / T >= 2 ? 2 : 1)
 primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
+    using L = LongSmem<T, CAP>;
+    extern __shared__ __align__(16) unsigned char lsm[];
+    double *s_u = reinterpret_cast<double *>(lsm + L::kU);
+    double *s_c = reinterpret_cast<double *>(lsm + L::kC);
+    int32_t *s_j = reinterpret_cast<int32_t *>(lsm + L::kJ);
+    uint8_t *s_f = lsm + L::kF;
     __shared__ double sm[96];
+    __shared__ int64_t claimed;
     const double tau = st.steps[0];
+    const int tid = threadIdx.x;
     int64_t my_sweeps = 0;
     int my_faults = 0;
-    // c = x - tau p[col] is kept in the row's x slots across the sweeps (one
-    // price gather per entry instead of one per sweep); every thread touches
-    // the same entries in every pass
-    double *__restrict__ cx = st.x;
     constexpr int LB = 4;
-    __shared__ int64_t claimed;
-    // rows (longest first) are claimed one at a time from a global counter
     for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) claimed = atomicAdd(st.blk_done + 1, 1);
+        __syncthreads();  // the previous row's shared-memory reads are done
+        if (tid == 0) claimed = atomicAdd(st.blk_done + 1, 1);
         __syncthreads();
         const int64_t r = claimed;
         if (r >= mk.nlong) break;
         const int64_t i = mk.long_rows[r];
-        const int64_t a = mk.row_ptr[i], b = mk.row_ptr[i + 1];
+        const int64_t a = mk.row_ptr[i];
+        const int len = (int)(mk.row_ptr[i + 1] - a);
+        const int ns = len < CAP ? len : CAP;
         const double tw = tau * mk.w[i];
+        double *__restrict__ gx = st.x + a;
         double s0 = 0.0, A = 0.0, B = 0.0;
-        for (int64_t t0 = a + threadIdx.x; t0 < b; t0 += LB * blockDim.x) {
-            double xv[LB], pv[LB];
+        for (int k0 = tid; k0 < len; k0 += LB * T) {
+            int jv[LB];
+            bool fv[LB];
+            double uv[LB], pv[LB], xv[LB];
 #pragma unroll
-            for (int q = 0; q < LB; ++q) {  // all loads of the batch before its stores
-                const int64_t t = t0 + q * blockDim.x;
-                xv[q] = t < b ? cx[t] : 0.0;
-                pv[q] = t < b ? __ldg(st.p + mk.col[t]) : 0.0;
+            for (int q = 0; q < LB; ++q) {  // every load of the batch before any store
+                const int k = k0 + q * T;
+                const bool in = k < len;
+                jv[q] = in ? __ldg(mk.col + a + k) : 0;
+                fv[q] = in && __ldg(st.xflag + a + k);
+                uv[q] = in ? __ldg(mk.u + a + k) : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < LB; ++q) {
-                const int64_t t = t0 + q * blockDim.x;
-                if (t < b) {
-                    const double ue = mk.u[t], ce = xv[q] - tau * pv[q];
-                    if (x_prev_out) x_prev_out[t] = xv[q];
-                    cx[t] = ce;
-                    s0 += ue * xv[q];
-                    A += ue * ce;
-                    B += ue * ue;
+                const int k = k0 + q * T;
+                pv[q] = k < len ? __ldg(st.p + jv[q]) : 0.0;
+                // past the cap the x slots carry c: read them whole
+                xv[q] = (fv[q] || (k >= CAP && k < len)) ? __ldcg(gx + k) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                const int k = k0 + q * T;
+                if (k < len) {
+                    const double ce = xv[q] - tau * pv[q];
+                    if (x_prev_out) x_prev_out[a + k] = xv[q];
+                    if (k < CAP) {
+                        s_u[k] = uv[q];
+                        s_c[k] = ce;
+                        s_j[k] = jv[q];
+                        s_f[k] = fv[q];
+                    } else {
+                        gx[k] = ce;
+                    }
+                    s0 += uv[q] * xv[q];
+                    A += uv[q] * ce;
+                    B += uv[q] * uv[q];
                 }
             }
         }
         block_sum3(s0, A, B, sm);
         double s = active_root(A, B, tw);
-        int prev_cnt = (int)(b - a);
+        int prev_cnt = len;
         int sweeps = 0;
         bool done = false;
         auto sweep = [&](double q, double &As, double &Bs, double &cnt) {
             As = 0.0;
             Bs = 0.0;
             cnt = 0.0;
-            for (int64_t t = a + threadIdx.x; t < b; t += blockDim.x) {
-                const double ue = mk.u[t];
-                const double ce = cx[t];
+            for (int k = tid; k < ns; k += T) {
+                const double ue = s_u[k], ce = s_c[k];
+                if (fma(ce, q, tw * ue) > 0.0) {
+                    As += ue * ce;
+                    Bs += ue * ue;
+                    cnt += 1.0;
+                }
+            }
+            for (int k = CAP + tid; k < len; k += T) {
+                const double ue = __ldg(mk.u + a + k), ce = gx[k];
                 if (fma(ce, q, tw * ue) > 0.0) {
                     As += ue * ce;
                     Bs += ue * ue;
@@ -782,32 +834,123 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
                 prev_cnt = cnt;
             }
         }
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             my_sweeps += sweeps;
             if (!done) ++my_faults;
             st.srow[i] = s;
         }
         const double inv_s = 1.0 / s;
-        for (int64_t t0 = a + threadIdx.x; t0 < b; t0 += LB * blockDim.x) {
-            double cv[LB];
+        for (int k = tid; k < ns; k += T)
+            put_x(mk, st, a + k, s_j[k], fmax(s_c[k] + tw * s_u[k] * inv_s, 0.0), s_f[k]);
+        for (int k0 = CAP + tid; k0 < len; k0 += LB * T) {
+            double cv[LB], uv[LB];
+            int jv[LB];
 #pragma unroll
             for (int q = 0; q < LB; ++q) {
-                const int64_t t = t0 + q * blockDim.x;
-                cv[q] = t < b ? cx[t] : 0.0;
+                const int k = k0 + q * T;
+                const bool in = k < len;
+                cv[q] = in ? gx[k] : 0.0;
+                uv[q] = in ? __ldg(mk.u + a + k) : 0.0;
+                jv[q] = in ? __ldg(mk.col + a + k) : 0;
             }
 #pragma unroll
             for (int q = 0; q < LB; ++q) {
-                const int64_t t = t0 + q * blockDim.x;
-                if (t < b) put_x(mk, st, t, mk.col[t], fmax(cv[q] + tw * mk.u[t] * inv_s, 0.0), true);
+                const int k = k0 + q * T;
+                if (k < len)  // the x slot held c: rewrite it
+                    put_x(mk, st, a + k, jv[q], fmax(cv[q] + tw * uv[q] * inv_s, 0.0), true);
             }
         }
-        __syncthreads();
     }
     __shared__ int64_t red[32];
     const int64_t tot = block_sum_i64(my_sweeps, red);
-    if (threadIdx.x == 0 && tot) atomicAdd((unsigned long long *)(st.pass_out + it), (unsigned long long)tot);
+    if (tid == 0 && tot) atomicAdd((unsigned long long *)(st.pass_out + it), (unsigned long long)tot);
     const int64_t fl = block_sum_i64((int64_t)my_faults, red);
-    if (threadIdx.x == 0 && fl) atomicAdd((unsigned long long *)st.faults, (unsigned long long)fl);
+    if (tid == 0 && fl) atomicAdd((unsigned long long *)st.faults, (unsigned long long)fl);
+}
+
+// Medium rows (MQ_REG_ROW < length <= MQ_LONG_ROW, listed longest first in
+// mk.med_rows): one warp per row, rows claimed from a global counter.  c is
+// kept in the row's x slots across the sweeps (each lane re-reads only the
+// entries it wrote); u, col and the flags are read straight from global
+// memory, MQ_LB entries per lane in flight.
+__global__ void __launch_bounds__(256)
+primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
+    constexpr int G = 32, LB = MQ_LB;
+    const double tau = st.steps[0];
+    const int lane = threadIdx.x & 31;
+    int my_sweeps = 0, my_faults = 0;
+    for (;;) {
+        int r = 0;
+        if (lane == 0) r = atomicAdd(st.blk_done + 2, 1);
+        r = __shfl_sync(MQ_FULL, r, 0);
+        if (r >= mk.nmed) break;  // warp-uniform
+        const int64_t i = mk.med_rows[r];
+        const int64_t e0 = mk.row_ptr[i];
+        const int len = (int)(mk.row_ptr[i + 1] - e0);
+        const double tw = tau * mk.w[i];
+        const double *__restrict__ su = mk.u + e0;
+        const int32_t *__restrict__ cl = mk.col + e0;
+        const uint8_t *__restrict__ fl = st.xflag + e0;
+        double *sc = st.x + e0;
+        double s0p = 0.0, ap = 0.0, bp = 0.0;
+        for (int t0 = lane; t0 < len; t0 += LB * G) {
+            double pv[LB], xv[LB], uv[LB];
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {  // all loads of the batch before its stores
+                const int t = t0 + q * G;
+                const bool in = t < len;
+                pv[q] = in ? __ldg(st.p + __ldg(cl + t)) : 0.0;
+                xv[q] = (in && __ldg(fl + t)) ? __ldcg(sc + t) : 0.0;
+                uv[q] = in ? __ldg(su + t) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                const int t = t0 + q * G;
+                if (t < len) {
+                    const double ce = xv[q] - tau * pv[q];
+                    if (x_prev_out) x_prev_out[e0 + t] = xv[q];
+                    sc[t] = ce;  // this lane's entry only
+                    s0p += uv[q] * xv[q];
+                    ap += uv[q] * ce;
+                    bp += uv[q] * uv[q];
+                }
+            }
+        }
+        const double s0 = group_sum<G>(s0p);
+        const double A = group_sum<G>(ap);
+        const double B = group_sum<G>(bp);
+        int nsw = 0;
+        bool ok = true;
+        const double sr = row_root_exact<G>(su, sc, 0, len, lane, tw, s0, A, B, true, &nsw, &ok);
+        if (lane == 0) {
+            st.srow[i] = sr;
+            my_sweeps += nsw;
+            if (!ok) ++my_faults;
+        }
+        const double inv_s = 1.0 / sr;
+        for (int t0 = lane; t0 < len; t0 += LB * G) {
+            double cv[LB], uv[LB];
+            int jv[LB];
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                const int t = t0 + q * G;
+                const bool in = t < len;
+                cv[q] = in ? sc[t] : 0.0;
+                uv[q] = in ? __ldg(su + t) : 0.0;
+                jv[q] = in ? __ldg(cl + t) : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                const int t = t0 + q * G;
+                if (t < len)  // x held c: rewrite every entry
+                    put_x(mk, st, e0 + t, jv[q], fmax(cv[q] + tw * uv[q] * inv_s, 0.0), true);
+            }
+        }
+    }
+    if (lane == 0 && my_sweeps)
+        atomicAdd((unsigned long long *)(st.pass_out + it), (unsigned long long)my_sweeps);
+    if (lane == 0 && my_faults)
+        atomicAdd((unsigned long long *)st.faults, (unsigned long long)my_faults);
 }
 
 // ------------------------------------------------------------ column sums
@@ -904,9 +1047,24 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
                                                                    mk->ntiles, st->blk_done);
     }
     if (mk->nlong > 0) {
+        using LS = LongSmem<MQ_LONG_THREADS, MQ_LONG_CAP>;
+        auto lk = primal_long_kernel<MQ_LONG_THREADS, MQ_LONG_CAP>;
+        static bool lconfigured = false;
+        if (!lconfigured) {
+            cudaError_t e =
+                cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, LS::kBytes);
+            if (e != cudaSuccess) return set_error(e, "mq_primal_step: long-row smem attribute");
+            lconfigured = true;
+        }
         cudaMemsetAsync(st->blk_done + 1, 0, sizeof(int32_t), s);  // long-row counter
-        const int grid = grid_for(mk->nlong, 1, sm_count() * 8);
-        primal_long_kernel<<<grid, MQ_LONG_THREADS, 0, s>>>(*mk, *st, it, xprev);
+        const int per_sm = 2048 / MQ_LONG_THREADS >= 2 ? 2 : 1;
+        const int grid = grid_for(mk->nlong, 1, sm_count() * per_sm);
+        lk<<<grid, MQ_LONG_THREADS, LS::kBytes, s>>>(*mk, *st, it, xprev);
+    }
+    if (mk->nmed > 0) {
+        cudaMemsetAsync(st->blk_done + 2, 0, sizeof(int32_t), s);  // medium-row counter
+        const int grid = grid_for(mk->nmed, 8, sm_count() * 8);
+        primal_med_kernel<<<grid, 256, 0, s>>>(*mk, *st, it, xprev);
     }
     return check_launch("mq_primal_step");
 }
@@ -989,6 +1147,7 @@ int mq_debug_counters(unsigned long long *out_host) {
 }
 
 int mq_tile_entries(void) { return MQ_ETILE; }
+int mq_reg_row(void) { return MQ_REG_PER * MQ_G; }
 int mq_colsum_mode(void) { return 5; }   // fixed-point sparse column sums
 int mq_bucket_slots(void) { return 0; }  // no bucket mode in this build
 int mq_x_sparse(void) { return 1; }

@@ -5,6 +5,7 @@
     u_orig   float64 [nnz]        (residuals are measured on the original data)
     tiles    int64 [ntiles, 4]    (r0, r1, e0, e1): rows / entries of each tile
     long_rows int32 [nlong]       rows longer than 1024 entries
+    med_rows int32 [nmed]         tile rows longer than 128 entries (warp per row)
     bperm    int32 [nnz]          tile-blocked transpose schedule: per block of
     bptr     int32 [(nblk+1)m+1]  8 x prim_grid tiles, per good, ascending rows
                                   (pseudo-block nblk = the long rows)
@@ -82,6 +83,20 @@ def build_tiles(row_ptr, tile_entries=nat.TILE_ENTRIES, long_row=nat.LONG_ROW,
     last = torch.cat([starts[1:] - 1, torch.tensor([rows.numel() - 1], device=dev)])
     tiles = torch.stack([rows[starts], rows[last] + 1], 1).contiguous()
     return tiles, long_rows
+
+
+def medium_rows(row_ptr, long_rows, reg_row=nat.REG_ROW):
+    """Tile rows longer than reg_row (the register capacity of a tile row
+    solve), longest first: the warp-per-row kernel claims them in order.
+    Returns int32 [nmed]."""
+    lens = row_ptr[1:] - row_ptr[:-1]
+    med = lens > reg_row
+    if long_rows.numel():
+        med[long_rows.to(torch.int64)] = False
+    rows = torch.nonzero(med).flatten()
+    if rows.numel() > 1:
+        rows = rows[torch.argsort(lens[rows], descending=True, stable=True)]
+    return rows.to(torch.int32).contiguous()
 
 
 TILES_PER_CTA_PER_BLOCK = int(os.environ.get("MQ_TILES_PER_CTA", "4"))  # tuning override
@@ -204,6 +219,7 @@ class DeviceMarket:
                 order = torch.argsort(self.row_ptr[lr + 1] - self.row_ptr[lr], descending=True,
                                       stable=True)
                 self.long_rows = self.long_rows[order].contiguous()
+            self.med_rows = medium_rows(self.row_ptr, self.long_rows, int(self.lib.mq_reg_row()))
             # (r0, r1, e0, e1) per tile: the producer warp needs no dependent loads
             self.tiles = torch.cat([tiles2, self.row_ptr[tiles2]], 1).contiguous()
             self.prim_grid = int(min(max(1, self.tiles.shape[0]), sm_count(dev)))
@@ -241,6 +257,8 @@ class DeviceMarket:
         s.ntiles = int(self.tiles.shape[0])
         s.long_rows = self.long_rows.data_ptr()
         s.nlong = int(self.long_rows.numel())
+        s.med_rows = self.med_rows.data_ptr()
+        s.nmed = int(self.med_rows.numel())
         s.bperm = self.bperm.data_ptr()
         s.bptr = self.bptr.data_ptr()
         s.nblk = int(self.nblk)
@@ -264,7 +282,7 @@ class DeviceMarket:
 
     def bytes_resident(self):
         ts = [self._rp_buf, self._col_buf, self._u_buf, self.u_orig, self._w_buf, self.scales,
-              self.tiles, self.long_rows, self.bperm, self.bptr]
+              self.tiles, self.long_rows, self.med_rows, self.bperm, self.bptr]
         if self.tperm is not None:
             ts += [self.tperm, self.tptr]
         return sum(t.numel() * t.element_size() for t in ts)

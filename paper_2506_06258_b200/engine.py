@@ -217,8 +217,8 @@ class PdhcgEngine:
         # per-buyer utility of the last prox: the fused row solve's warm start
         self._srow_buf = torch.zeros(dm.n + nat.PAD, **f64)
         self.srow = self._srow_buf[:dm.n]
-        # the primal kernels' dynamic work counters (tiles, long rows)
-        self.blk_done = torch.zeros(2, dtype=torch.int32, device=dev)
+        # the primal kernels' dynamic work counters (tiles, long rows, medium rows)
+        self.blk_done = torch.zeros(3, dtype=torch.int32, device=dev)
         # fixed-point column sums: m u64 accumulators, zero between iterations
         fixed = getattr(getattr(dm, "lib", None), "mq_fixed_colsum", None)
         self.fixed = bool(fixed is not None and fixed() == 1 and self.mode != "ksection")

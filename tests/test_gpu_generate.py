@@ -82,3 +82,45 @@ def test_power_law_market_solves_like_the_oracle(oracle):
     assert np.max(np.abs(eng.x.cpu().numpy() - x)) <= 1e-10 * max(1.0, np.abs(x).max())
     assert np.max(np.abs(eng.p.cpu().numpy() - p)) <= 1e-11 * max(1.0, np.abs(p).max())
     assert np.max(np.abs(eng.xbar.cpu().numpy() - xb)) <= 1e-10 * max(1.0, np.abs(xb).max())
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_every_row_class_matches_the_oracle(oracle, seed):
+    """Register rows (<= 128 entries), medium rows (warp per row), long rows
+    held in shared memory and long rows past the shared-memory cap (c in the
+    x slots), interleaved in one market, against the oracle's k-section at
+    subtol 0 over several iterations."""
+    from paper_2506_06258_b200.device import DeviceMarket
+    from paper_2506_06258_b200.engine import PdhcgEngine
+
+    rng = np.random.default_rng(seed)
+    m = 12_000
+    lens = np.concatenate([rng.integers(1, 101, 300), rng.integers(129, 1025, 60),
+                           rng.integers(1025, 5001, 20),
+                           [5_119, 5_120, 5_121, 6_000, 10_239, 10_240, 10_241, 11_500, m]])
+    rng.shuffle(lens)
+    n = lens.size
+    rows = [np.sort(rng.choice(m, size=int(k), replace=False)) for k in lens]
+    rp = np.zeros(n + 1, dtype=np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = np.concatenate(rows).astype(np.int32)
+    u = rng.random(col.size)
+    u[u == 0.0] = 0.5
+    w = rng.random(n) + 0.01
+    dm = DeviceMarket(rp, col, u, w, m)
+    assert dm.long_rows.numel() == 29 and dm.med_rows.numel() == 60
+    eng = PdhcgEngine(dm)
+    eng.initial_state(w_sum=float(w.sum()))
+    eng.set_steps(0.05, 0.05)
+    x0 = eng.x.cpu().numpy().copy()
+    p0 = eng.p.cpu().numpy().copy()
+    eng.run_chunk(6)
+    mk = oracle.Market(n, m, rp, col, u, w)
+    nm, _ = oracle.normalize(mk)
+    tperm, tind = oracle.transpose_schedule(nm)
+    x, xp, p, xb, pb = x0.copy(), x0.copy(), p0.copy(), x0.copy(), p0.copy()
+    oracle.pdhcg_chunk(nm.indptr, nm.col, nm.val, tperm, tind, nm.w, x, xp, p, xb, pb, 0, 0.05,
+                       0.05, 32, 0.0, 6, np.empty(nm.nnz), np.zeros(6, dtype=np.int64))
+    assert np.max(np.abs(eng.x.cpu().numpy() - x)) <= 1e-10 * max(1.0, np.abs(x).max())
+    assert np.max(np.abs(eng.p.cpu().numpy() - p)) <= 1e-11 * max(1.0, np.abs(p).max())
+    assert np.max(np.abs(eng.xbar.cpu().numpy() - xb)) <= 1e-10 * max(1.0, np.abs(xb).max())

@@ -24,7 +24,7 @@ def test_native_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(lib, name)
-    assert lib.mq_abi_version() == 6
+    assert lib.mq_abi_version() == 7
     assert lib.mq_scratch_doubles() > 0
 
 
@@ -173,6 +173,7 @@ def test_abi_marshaling_without_device():
         "mq_normalize_rows": (0, None, None, None, None, None),
         "mq_gen_degrees": (0, 1, 10, 0, 0.5, 2.0, 1.0, 1, None, None),
         "mq_tile_entries": (),
+        "mq_reg_row": (),
         "mq_colsum_mode": (),
         "mq_fixed_colsum": (),
         "mq_x_sparse": (),
@@ -190,7 +191,7 @@ def test_abi_marshaling_without_device():
             assert rc >= 0
             continue
         assert rc != 0, name
-        if name in ("mq_tile_entries", "mq_colsum_mode"):
+        if name in ("mq_tile_entries", "mq_reg_row"):
             continue
         assert lib.mq_last_error()
 
