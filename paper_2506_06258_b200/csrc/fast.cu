@@ -715,7 +715,7 @@ struct LongSmem {
 };
 
 template <int T, int CAP>
-__global__ void __launch_bounds__(T, 2048 / T >= 2 ? 2 : 1)
+__global__ void __launch_bounds__(T, T <= 512 ? 2 : 1)
 primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
     using L = LongSmem<T, CAP>;
     extern __shared__ __align__(16) unsigned char lsm[];
@@ -1040,12 +1040,11 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
         if (e != cudaSuccess) return set_error(e, "mq_primal_step: smem attribute");
         configured = true;
     }
-    if (mk->ntiles > 0) {
-        // the dynamic tile counter lives in blk_done[0] (zeroed per launch)
-        cudaMemsetAsync(st->blk_done, 0, sizeof(int32_t), s);
+    // every dynamic work counter (tiles, long rows, medium rows) restarts at 0
+    cudaMemsetAsync(st->blk_done, 0, 3 * sizeof(int32_t), s);
+    if (mk->ntiles > 0)  // the dynamic tile counter lives in blk_done[0]
         kern<<<mk->prim_grid, (MQ_NSW + 1) * 32, kPrimalSmem, s>>>(*mk, *st, it, xprev, 0,
                                                                    mk->ntiles, st->blk_done);
-    }
     if (mk->nlong > 0) {
         using LS = LongSmem<MQ_LONG_THREADS, MQ_LONG_CAP>;
         auto lk = primal_long_kernel<MQ_LONG_THREADS, MQ_LONG_CAP>;
@@ -1056,13 +1055,11 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
             if (e != cudaSuccess) return set_error(e, "mq_primal_step: long-row smem attribute");
             lconfigured = true;
         }
-        cudaMemsetAsync(st->blk_done + 1, 0, sizeof(int32_t), s);  // long-row counter
-        const int per_sm = 2048 / MQ_LONG_THREADS >= 2 ? 2 : 1;
+        const int per_sm = MQ_LONG_THREADS <= 512 ? 2 : 1;
         const int grid = grid_for(mk->nlong, 1, sm_count() * per_sm);
         lk<<<grid, MQ_LONG_THREADS, LS::kBytes, s>>>(*mk, *st, it, xprev);
     }
     if (mk->nmed > 0) {
-        cudaMemsetAsync(st->blk_done + 2, 0, sizeof(int32_t), s);  // medium-row counter
         const int grid = grid_for(mk->nmed, 8, sm_count() * 8);
         primal_med_kernel<<<grid, 256, 0, s>>>(*mk, *st, it, xprev);
     }
