@@ -346,7 +346,8 @@ def main():
     # kernels launched in the timed region: dual + non-empty primal bins + colsum
     # per iteration, chunk_end (+ the running-average materialization) per chunk
     # (+ finalize on N>1)
-    primal_kernels = int(dm.tiles.shape[0] > 0) + int(dm.long_rows.numel() > 0)
+    primal_kernels = (int(dm.tiles.shape[0] > 0) + int(dm.long_rows.numel() > 0)
+                      + int(dm.med_rows.numel() > 0))
     per_it = 2 + primal_kernels + (1 if world > 1 else 0)
     launches = a.steps * per_it + -(-a.steps // 40) * (1 + int(eng.sparse))
 
@@ -377,7 +378,8 @@ def main():
                    "l2": f"inputs larger than L2 ({iter_bytes / 1e9:.1f} GB algorithmic "
                          "traffic per iteration vs 126 MB L2)"},
         "roofline": {"bound": "hbm",
-                     "kernel": "primal_fused_kernel (exact prox + averages + column sums)",
+                     "kernel": "primal step: primal_fused_kernel (exact prox + averages + "
+                               "column sums) + medium / long row kernels where present",
                      "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(achieved / hbm_peak, 4),
                      "traffic": traffic, "peak_kind": peak_kind,

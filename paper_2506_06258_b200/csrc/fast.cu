@@ -62,8 +62,12 @@
 #ifndef MQ_LONG_THREADS
 #define MQ_LONG_THREADS 512  // threads per CTA of the long-row kernel (one row per CTA)
 #endif
+#ifndef MQ_LONG_LB
+#define MQ_LONG_LB 4  // entries per thread batched ahead of the stores (long rows)
+#endif
 #ifndef MQ_LONG_CAP
-#define MQ_LONG_CAP 5120  // entries of a long row kept in shared memory (107.5 KB, 2 CTAs/SM)
+#define MQ_LONG_CAP 3072  // entries of a long row kept in shared memory (64.5 KB, 2 CTAs/SM:
+                          // the rest of the carveout stays L1 for the price gathers)
 #endif
 
 namespace mq {
@@ -729,7 +733,7 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
     const int tid = threadIdx.x;
     int64_t my_sweeps = 0;
     int my_faults = 0;
-    constexpr int LB = 4;
+    constexpr int LB = MQ_LONG_LB;
     for (;;) {
         __syncthreads();  // the previous row's shared-memory reads are done
         if (tid == 0) claimed = atomicAdd(st.blk_done + 1, 1);
