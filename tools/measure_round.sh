@@ -15,7 +15,7 @@ timeout 900 python bench.py --impl reference > $O/bench_ref_$TAG.log 2>&1
 echo "ref rc=$?" >> $O/status_$TAG.txt
 timeout 600 python bench.py --config c3 --no-cpu > $O/bench_c3_$TAG.log 2>&1
 echo "c3 rc=$?" >> $O/status_$TAG.txt
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2500 --csv \
   --log-file $O/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > $O/ncu_l_$TAG.log 2>&1
 echo "ncu-list rc=$?" >> $O/status_$TAG.txt
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:primal_fused -s 3 -c 1 \
@@ -26,4 +26,6 @@ if [ -z "$2" ]; then
   echo "ttt2 rc=$?" >> $O/status_$TAG.txt
   timeout 1500 python tools/ttt.py c4 > $O/ttt_c4_$TAG.log 2>&1
   echo "ttt4 rc=$?" >> $O/status_$TAG.txt
+  timeout 600 python tools/ttt.py c3 > $O/ttt_c3_$TAG.log 2>&1
+  echo "ttt3 rc=$?" >> $O/status_$TAG.txt
 fi
