@@ -60,13 +60,16 @@
 #define MQ_LB 8  // entries per lane batched ahead of the stores (longer rows)
 #endif
 #ifndef MQ_LONG_THREADS
-#define MQ_LONG_THREADS 512  // threads per CTA of the long-row kernel (one row per CTA)
+#define MQ_LONG_THREADS 256  // threads per CTA of the long-row kernel (one row per CTA)
+#endif
+#ifndef MQ_LONG_PER_SM
+#define MQ_LONG_PER_SM 4  // resident long-row CTAs per SM (one row each)
 #endif
 #ifndef MQ_LONG_LB
 #define MQ_LONG_LB 4  // entries per thread batched ahead of the stores (long rows)
 #endif
 #ifndef MQ_LONG_CAP
-#define MQ_LONG_CAP 3072  // entries of a long row kept in shared memory (64.5 KB, 2 CTAs/SM:
+#define MQ_LONG_CAP 1536  // entries of a long row kept in shared memory (32 KB, 4 CTAs/SM:
                           // the rest of the carveout stays L1 for the price gathers)
 #endif
 
@@ -679,26 +682,30 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
         atomicAdd((unsigned long long *)st.faults, (unsigned long long)my_faults);
 }
 
-// Long rows (> MQ_LONG_ROW entries): one CTA per row; every sweep re-reads
-// the row (L1/L2 resident).
-__device__ __forceinline__ void block_sum3(double &a, double &b, double &c, double *sm /*[96]*/) {
+// Sums of three values over the CTA, every thread gets the totals.  Two
+// slot buffers alternate (phase), so one barrier per call suffices: a
+// buffer is rewritten two calls later, after every thread has passed the
+// barrier of the call in between.
+__device__ __forceinline__ void block_sum3(double &a, double &b, double &c, double *sm /*[192]*/,
+                                           int &phase) {
     a = group_sum<32>(a);
     b = group_sum<32>(b);
     c = group_sum<32>(c);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nw = blockDim.x >> 5;
-    __syncthreads();
+    double *buf = sm + 96 * (phase & 1);
+    ++phase;
     if (lane == 0) {
-        sm[warp] = a;
-        sm[32 + warp] = b;
-        sm[64 + warp] = c;
+        buf[warp] = a;
+        buf[32 + warp] = b;
+        buf[64 + warp] = c;
     }
     __syncthreads();
     double ra = 0.0, rb = 0.0, rc = 0.0;
     if (lane < nw) {
-        ra = sm[lane];
-        rb = sm[32 + lane];
-        rc = sm[64 + lane];
+        ra = buf[lane];
+        rb = buf[32 + lane];
+        rc = buf[64 + lane];
     }
     a = group_sum<32>(ra);
     b = group_sum<32>(rb);
@@ -719,7 +726,7 @@ struct LongSmem {
 };
 
 template <int T, int CAP>
-__global__ void __launch_bounds__(T, T <= 512 ? 2 : 1)
+__global__ void __launch_bounds__(T, MQ_LONG_PER_SM)
 primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
     using L = LongSmem<T, CAP>;
     extern __shared__ __align__(16) unsigned char lsm[];
@@ -727,8 +734,9 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
     double *s_c = reinterpret_cast<double *>(lsm + L::kC);
     int32_t *s_j = reinterpret_cast<int32_t *>(lsm + L::kJ);
     uint8_t *s_f = lsm + L::kF;
-    __shared__ double sm[96];
+    __shared__ double sm[192];
     __shared__ int64_t claimed;
+    int phase = 0;
     const double tau = st.steps[0];
     const int tid = threadIdx.x;
     int64_t my_sweeps = 0;
@@ -786,7 +794,7 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
                 }
             }
         }
-        block_sum3(s0, A, B, sm);
+        block_sum3(s0, A, B, sm, phase);
         double s = active_root(A, B, tw);
         int prev_cnt = len;
         int sweeps = 0;
@@ -811,7 +819,7 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
                     cnt += 1.0;
                 }
             }
-            block_sum3(As, Bs, cnt, sm);
+            block_sum3(As, Bs, cnt, sm, phase);
         };
         if (s0 > s) {
             double A0, B0, k0;
@@ -1059,7 +1067,7 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
             if (e != cudaSuccess) return set_error(e, "mq_primal_step: long-row smem attribute");
             lconfigured = true;
         }
-        const int per_sm = MQ_LONG_THREADS <= 512 ? 2 : 1;
+        const int per_sm = MQ_LONG_PER_SM;
         const int grid = grid_for(mk->nlong, 1, sm_count() * per_sm);
         lk<<<grid, MQ_LONG_THREADS, LS::kBytes, s>>>(*mk, *st, it, xprev);
     }

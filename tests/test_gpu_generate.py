@@ -97,7 +97,7 @@ def test_every_row_class_matches_the_oracle(oracle, seed):
     m = 12_000
     lens = np.concatenate([rng.integers(1, 101, 300), rng.integers(129, 1025, 60),
                            rng.integers(1025, 5001, 20),
-                           [3_071, 3_072, 3_073, 5_119, 5_120, 5_121, 6_000, 10_239, 10_240,
+                           [1_535, 1_536, 1_537, 3_071, 3_072, 3_073, 5_119, 5_120, 5_121, 6_000, 10_239, 10_240,
                             10_241, 11_500, m]])
     rng.shuffle(lens)
     n = lens.size
@@ -109,7 +109,7 @@ def test_every_row_class_matches_the_oracle(oracle, seed):
     u[u == 0.0] = 0.5
     w = rng.random(n) + 0.01
     dm = DeviceMarket(rp, col, u, w, m)
-    assert dm.long_rows.numel() == 32 and dm.med_rows.numel() == 60
+    assert dm.long_rows.numel() == 35 and dm.med_rows.numel() == 60
     eng = PdhcgEngine(dm)
     eng.initial_state(w_sum=float(w.sum()))
     eng.set_steps(0.05, 0.05)
