@@ -885,9 +885,16 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
 // kept in the row's x slots across the sweeps (each lane re-reads only the
 // entries it wrote); u, col and the flags are read straight from global
 // memory, MQ_LB entries per lane in flight.
+#ifndef MQ_MED_LB
+#define MQ_MED_LB MQ_LB  // entries per lane batched ahead of the stores (medium rows)
+#endif
+#ifdef MQ_MED_MINB  // tuning: resident 256-thread CTAs per SM to build for
+__global__ void __launch_bounds__(256, MQ_MED_MINB)
+#else
 __global__ void __launch_bounds__(256)
+#endif
 primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
-    constexpr int G = 32, LB = MQ_LB;
+    constexpr int G = 32, LB = MQ_MED_LB;
     const double tau = st.steps[0];
     const int lane = threadIdx.x & 31;
     int my_sweeps = 0, my_faults = 0;

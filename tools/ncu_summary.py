@@ -80,7 +80,7 @@ md += ["", "## Launch list (ncu, cold-cache, serialised)", "", "| kernel | launc
        "|---|---|---|---|"]
 for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
     md.append(f"| {k} | {cnt[k]} | {v:.3f} | {100 * v / S:.1f}% |")
-ITER = ("primal_fused", "dual_kernel", "colsum_finalize", "chunk_end", "colsum_blocks", "primal_long")
+ITER = ("primal_fused", "dual_kernel", "colsum_finalize", "chunk_end", "colsum_blocks", "primal_long", "primal_med", "cs_from_fixed")
 it = {k: v for k, v in tot.items() if any(t in k for t in ITER)}
 SI = sum(it.values()) or 1.0
 md += ["", "## Per-iteration kernels only (the bench's timed region)", "",
