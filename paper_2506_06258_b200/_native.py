@@ -14,7 +14,7 @@ from .errors import MarketError
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MQ_LIB") or os.path.join(_PKG, "libmarket_eq_b200.so")
 TILE_ENTRIES = 2560   # MQ_TILE_ENTRIES
-LONG_ROW = 1024       # MQ_LONG_ROW
+LONG_ROW = int(os.environ.get("MQ_LONG_ROW", "1024"))  # MQ_LONG_ROW (tuning override)
 REG_ROW = 128         # MQ_REG_ROW
 TILE_ROWS = 256       # MQ_TILE_ROWS
 PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
