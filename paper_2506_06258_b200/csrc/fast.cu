@@ -29,6 +29,11 @@
 //    counts, claiming tiles dynamically from a global counter;
 //  * 19 solver warps claim row pairs of the current tile (two 16-lane groups
 //    per warp) and solve them, rows of <= 128 entries in registers.
+// Skewed markets add two kernels after it: tile rows of 129-1024 entries
+// (skipped by the tile kernel, so no stage waits on one slow row) are solved
+// one warp per row (primal_med_kernel), rows > 1024 entries one CTA per row
+// with the row's first MQ_LONG_CAP entries held in shared memory across the
+// sweeps (primal_long_kernel).
 // Variants measured along the way (dense iterate with gathered / bucketed /
 // scattered column sums, gather warps, software pipelining, ...) are listed
 // with their numbers in DESIGN.md §11.
