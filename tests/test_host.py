@@ -231,6 +231,33 @@ def test_primal_tiles_cover_rows_once():
         assert set(long_rows.tolist()) == set(np.flatnonzero(lens > 1024).tolist())
 
 
+def test_tiles_are_greedy_and_medium_rows_listed():
+    """Each tile ends only where the next row would overflow it (entries or
+    rows) or is long; medium rows are the tile rows above the register
+    capacity, longest first."""
+    import torch
+
+    from paper_2506_06258_b200.device import build_tiles, medium_rows
+
+    rng = np.random.default_rng(3)
+    lens = np.concatenate([rng.poisson(30, 4000), rng.integers(129, 1025, 300),
+                           rng.integers(1025, 3000, 40)]).astype(np.int64)
+    rng.shuffle(lens)
+    rp = np.zeros(len(lens) + 1, dtype=np.int64)
+    rp[1:] = np.cumsum(lens)
+    rpt = torch.from_numpy(rp)
+    tiles, long_rows = build_tiles(rpt, 2560, 1024, 256)
+    tiles = tiles.numpy()
+    for r0, r1 in tiles:
+        assert rp[r1] - rp[r0] <= 2560 and r1 - r0 <= 256
+        if r1 < len(lens) and lens[r1] <= 1024:
+            assert rp[r1 + 1] - rp[r0] > 2560 or r1 + 1 - r0 > 256
+    med = medium_rows(rpt, long_rows, 128).numpy()
+    want = np.flatnonzero((lens > 128) & (lens <= 1024))
+    assert sorted(med.tolist()) == want.tolist()
+    assert np.all(np.diff(lens[med]) <= 0)
+
+
 def test_blocked_schedule_preserves_column_order():
     """Walking a good block by block (tiles, then the long-row pseudo-block)
     visits its tile entries in ascending row order, and every entry once."""
