@@ -109,7 +109,9 @@ def test_every_row_class_matches_the_oracle(oracle, seed):
     u[u == 0.0] = 0.5
     w = rng.random(n) + 0.01
     dm = DeviceMarket(rp, col, u, w, m)
-    assert dm.long_rows.numel() == 35 and dm.med_rows.numel() == 60
+    reg_row = int(dm.lib.mq_reg_row())
+    assert dm.long_rows.numel() == 35
+    assert dm.med_rows.numel() == int(np.sum((lens > reg_row) & (lens <= 1024)))
     eng = PdhcgEngine(dm)
     eng.initial_state(w_sum=float(w.sum()))
     eng.set_steps(0.05, 0.05)
