@@ -231,47 +231,47 @@ def traffic_from_profile(name, config):
 
 # ------------------------------------------------------------------ CPU side
 
-def host_sample(shard, target_nnz):
-    """First rows of the market with ~target_nnz entries, as host arrays."""
-    rp = shard["row_ptr"]
-    rows = int(np.searchsorted(rp.cpu().numpy(), target_nnz, side="right")) - 1
-    rows = max(1, min(rows, rp.numel() - 1))
-    nnz = int(rp[rows].item())
-    return (rp[:rows + 1].cpu().numpy(), shard["col"][:nnz].cpu().numpy().astype(np.int64),
-            shard["u"][:nnz].cpu().numpy(), shard["w"][:rows].cpu().numpy())
+def host_copy(shard):
+    """Host arrays of this rank's shard (the e2e input and the CPU legs)."""
+    from paper_2506_06258_b200.engine import to_host
+
+    return {"row_ptr": shard["row_ptr"].cpu().numpy(), "col": to_host(shard["col"]),
+            "u": to_host(shard["u"]), "w": shard["w"].cpu().numpy(), "n": shard["n"],
+            "m": shard["m"]}
 
 
-def cpu_iteration_rate(sample, m, nnz_full, tau, sigma, iters, threads):
-    """Oracle (C restatement of kernels.pdhcg_chunk) on the sample; returns
-    (full-market iterations/s extrapolated by nnz, seconds per sample iteration)."""
+def cpu_chunk_run(host, threads):
+    """The reference's compact iterate on the FULL market on the host cores:
+    oracle.solve.ChunkRun = _CompactRun's setup (normalize, transpose
+    schedule, x = 1/colcount, p = sum(w)/m, L, omega_0 -> the first restart
+    window's tau/sigma) around the C restatement of kernels.pdhcg_chunk
+    (k-section 32, subproblem_tol 1e-10: the reference defaults)."""
     from oracle import solve as orc
 
-    rp, col, u, w = sample
     orc.set_threads(threads)
-    mk = orc.Market(len(rp) - 1, m, rp, col, u, w)
-    nm, _ = orc.normalize(mk)
-    tperm, tind = orc.transpose_schedule(nm)
-    counts = np.bincount(nm.col, minlength=m).astype(np.float64)
-    x = 1.0 / np.maximum(counts, 1.0)[nm.col]
-    p = np.full(m, float(np.sum(w)) / m)
-    xp, xb, pb = x.copy(), x.copy(), p.copy()
-    cbuf = np.empty(nm.nnz)
-    col32, tp32 = nm.col.astype(np.int32), tperm.astype(np.int32)
-    passes = np.zeros(1, dtype=np.int64)
-    orc.pdhcg_chunk(nm.indptr, col32, nm.val, tp32, tind, nm.w, x, xp, p, xb, pb, 0, tau, sigma,
-                    32, 1e-10, 1, cbuf, passes)  # warm-up
     t0 = time.perf_counter()
-    passes = np.zeros(iters, dtype=np.int64)
-    orc.pdhcg_chunk(nm.indptr, col32, nm.val, tp32, tind, nm.w, x, xp, p, xb, pb, 1, tau, sigma,
-                    32, 1e-10, iters, cbuf, passes)
+    run = orc.ChunkRun(host["row_ptr"], host["col"], host["u"], host["w"], host["m"])
+    return run, time.perf_counter() - t0
+
+
+def cpu_baseline(host, iters=1):
+    """Reported CPU baseline: `iters` iterations of the reference algorithm
+    over the whole market from its initial state (no sample, no
+    extrapolation)."""
+    threads = os.cpu_count() or 1
+    run, setup = cpu_chunk_run(host, threads)
+    t0 = time.perf_counter()
+    passes = run.step(iters)
     dt = (time.perf_counter() - t0) / iters
-    return (nm.nnz / nnz_full) / dt, dt, nm.nnz, len(rp) - 1
-
-
-def calibrated_sample_nnz(shard, m, nnz_full, tau, sigma, threads, seconds_per_iter):
-    probe = host_sample(shard, 1_000_000)
-    _, dt, nnz_probe, _ = cpu_iteration_rate(probe, m, nnz_full, tau, sigma, 1, threads)
-    return int(min(nnz_full, max(200_000, nnz_probe * seconds_per_iter / max(dt, 1e-6))))
+    nnz = int(host["row_ptr"][-1])
+    return {"value": round(1.0 / dt, 6), "unit": "iter/s", "cores": threads, "kind": "port",
+            "sample": f"{iters} iteration(s) of the whole market (n={host['n']}, m={host['m']}, "
+                      f"nnz={nnz}) from the initial state, C oracle = restated "
+                      f"kernels.pdhcg_chunk (k-section 32, subtol 1e-10), tau=sigma="
+                      f"{run.tau:.6g} (the solver's first restart window), {threads} threads; "
+                      f"{passes.sum() / max(1, host['n']) / iters:.2f} k-section passes per "
+                      f"row per iteration",
+            "seconds_per_iteration": round(dt, 4), "setup_seconds": round(setup, 2)}
 
 
 # ------------------------------------------------------------------ main
@@ -421,52 +421,50 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_solve(shard, max_iters):
-    """Full solve to 1e-4 through the public API from host buffers."""
+def e2e_solve(host, max_iters, group=None):
+    """Time to 1e-4 relative KKT through the public API: run_solve on a host
+    FisherInstance (upload, device setup, every residual check, the final
+    download), timed by the host clock around the call, plus the solve
+    loop alone as the reference's wall_time_seconds measures it
+    (driver.py:319,359)."""
     import torch
 
     import paper_2506_06258_b200 as mq
 
-    rp = shard["row_ptr"].cpu().numpy()
-    col = shard["col"].cpu().numpy().astype(np.int64)
-    u = shard["u"].cpu().numpy()
-    w = shard["w"].cpu().numpy()
-    inst = mq.FisherInstance(mq.SparseMatrix(shard["n"], shard["m"], rp, col, u), w)
-    del col, u
+    n, m = host["n"], host["m"]
+    inst = mq.FisherInstance(mq.SparseMatrix(host["row_ptr"].shape[0] - 1, m, host["row_ptr"],
+                                             host["col"], host["u"]), host["w"])
+    cfg = mq.SolveConfig(tol=1e-4, max_iters=max_iters, group=group)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rep = mq.run_solve(inst, mq.SolveConfig(tol=1e-4, max_iters=max_iters), "pdhcg")
+    rep = mq.run_solve(inst, cfg, "pdhcg")
     wall = time.perf_counter() - t0
-    nnz, n, m = inst.utilities.nnz, inst.n_buyers, inst.n_goods
-    h2d = 8 * (n + 1) + 4 * nnz + 8 * nnz + 8 * n
-    d2h = 8 * m + 8 * nnz + 8 * n + 8 * n
+    nnz, nl = inst.utilities.nnz, inst.n_buyers
+    # copies made by the call: row offsets, columns (int64), values, budgets
+    # up; prices, allocation, utility values and budgets back (+ 32 doubles
+    # of residual scalars per check)
+    h2d = 8 * (nl + 1) + 8 * nnz + 8 * nnz + 8 * nl
+    checks = len(rep.residual_history)
+    d2h = 8 * m + 8 * nnz + 8 * nl + 8 * nl + 8 * 32 * (checks + 2)
     its = rep.inner_iterations
     return {"value": round(its / wall, 3), "unit": "iter/s",
             "h2d_bytes_per_step": h2d // max(its, 1), "d2h_bytes_per_step": d2h // max(its, 1),
-            "ttt_seconds": round(wall, 3), "iterations": its, "restarts": rep.restarts,
-            "status": rep.status, "rel_kkt": rep.final_residuals.rel_kkt,
-            "objective": rep.objective,
+            "ttt_seconds": round(wall, 3), "solve_loop_seconds": round(rep.wall_time_seconds, 3),
+            "iterations": its, "restarts": rep.restarts, "status": rep.status,
+            "rel_kkt": rep.final_residuals.rel_kkt, "objective": rep.objective,
+            "checks": checks,
             "device_iters_per_second": round(rep.device_stats["iters_per_second"], 3),
-            "note": "one run_solve(tol=1e-4) on a host FisherInstance; per-step bytes = "
-                    "instance upload + result download amortized over the iterations"}
-
-
-def cpu_baseline(shard, m, nnz_full, seconds_per_iter=4.0, iters=3):
-    threads = os.cpu_count() or 1
-    tau = sigma = 0.9 / np.sqrt(float(nnz_full) / m)  # representative step sizes
-    target = calibrated_sample_nnz(shard, m, nnz_full, tau, sigma, threads, seconds_per_iter)
-    sample = host_sample(shard, target)
-    rate, dt, nnz_s, rows = cpu_iteration_rate(sample, m, nnz_full, tau, sigma, iters, threads)
-    return {"value": round(rate, 6), "unit": "iter/s", "cores": threads, "kind": "port",
-            "sample": f"first {rows} buyers ({nnz_s} nnz, {100.0 * nnz_s / nnz_full:.2f}% of "
-                      f"the market) x {iters} iterations of the C oracle "
-                      f"(kernels.pdhcg_chunk restatement, k-section 32, subtol 1e-10); "
-                      f"{dt:.3f} s/iteration on the sample, extrapolated linearly in nnz",
-            "seconds_per_sample_iteration": round(dt, 4)}
+            "note": "one run_solve(tol=1e-4) on a host FisherInstance, max_iters = "
+                    f"{max_iters} (the reference default); value = iterations / wall time "
+                    "of the call; per-step bytes = upload + download amortized"}
 
 
 def reference_arm(a, rank, world):
-    """The reference algorithm (C oracle port) on the host cores, rank 0 only."""
+    """--impl reference: the reference algorithm (oracle port of
+    kernels.pdhcg_chunk around _CompactRun's setup) on the host cores, on
+    the same market (regenerated on the host byte for byte by
+    oracle/market_gen.c; the product's CUDA library is never loaded), every
+    step one iteration of the whole market.  Rank 0 only."""
     import torch.distributed as dist
 
     if rank != 0:
@@ -474,41 +472,46 @@ def reference_arm(a, rank, world):
             dist.barrier()
             dist.destroy_process_group()
         return
-    import torch
-
-    from paper_2506_06258_b200 import _build
-
-    _build.build()
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
-    shard = shard_rows(a.config, 0, 1, a.seed)
-    n, m = shard["n"], shard["m"]
-    nnz_full = int(shard["row_ptr"][-1].item())
+    from oracle import gen as hg
+
     threads = os.cpu_count() or 1
-    tau = sigma = 0.9 / np.sqrt(float(nnz_full) / m)
-    # size one step so that warmup + steps fit in ~2 minutes
-    per_step = max(0.05, 120.0 / (a.steps + a.warmup))
-    target = calibrated_sample_nnz(shard, m, nnz_full, tau, sigma, threads, per_step)
-    sample = host_sample(shard, target)
-    del shard
-    torch.cuda.empty_cache()
-    cpu_iteration_rate(sample, m, nnz_full, tau, sigma, a.warmup, threads)
-    rate, dt, nnz_s, rows = cpu_iteration_rate(sample, m, nnz_full, tau, sigma, a.steps, threads)
+    t0 = time.perf_counter()
+    host = hg.generate_config(a.config, seed=a.seed, threads=threads)
+    gen_s = time.perf_counter() - t0
+    n, m = host["n"], host["m"]
+    nnz = int(host["row_ptr"][-1])
+    run, setup_s = cpu_chunk_run(host, threads)
+    del host
+    for _ in range(a.warmup):
+        run.step(1)
+    times, passes = [], 0
+    for _ in range(a.steps):
+        t1 = time.perf_counter()
+        passes += int(run.step(1).sum())
+        times.append(time.perf_counter() - t1)
+    total = sum(times)
+    rate = a.steps / total
     out = {
         "metric": METRIC, "value": round(rate, 6), "unit": "iter/s", "n_gpus": world,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 / rate, 3),
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 * total / a.steps, 3),
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": f"BASELINE config {a.config[1]}: {CONFIG_TEXT[a.config]}",
-                   "n_buyers": n, "m_goods": m, "nnz": nnz_full, "seed": a.seed,
-                   "row_solver": "ksection"},
+                   "n_buyers": n, "m_goods": m, "nnz": nnz, "seed": a.seed,
+                   "row_solver": "ksection (sections 32, subproblem_tol 1e-10)",
+                   "tau": run.tau, "sigma": run.sigma},
         "cpu_baseline": {"value": round(rate, 6), "unit": "iter/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"each step = one iteration of the C oracle "
-                                   f"(kernels.pdhcg_chunk restatement) over the first {rows} "
-                                   f"buyers ({nnz_s} nnz), extrapolated linearly in nnz to "
-                                   f"the full market"},
+                         "sample": f"the whole market every step: iterations {a.warmup + 1}.."
+                                   f"{a.warmup + a.steps} from the initial state of the C "
+                                   "oracle (restated kernels.pdhcg_chunk, bit-identical to the "
+                                   "reference's numba kernel), tau/sigma of the solver's first "
+                                   "restart window"},
         "e2e": {"value": round(rate, 6), "unit": "iter/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "passes_per_row_per_iteration": round(passes / a.steps / n, 3),
+        "generate_seconds": round(gen_s, 2), "setup_seconds": round(setup_s, 2),
     }
     print(json.dumps(out), flush=True)
     if world > 1:

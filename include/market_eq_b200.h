@@ -32,12 +32,13 @@
 extern "C" {
 #endif
 
-#define MQ_ABI_VERSION 7
+#define MQ_ABI_VERSION 8
 #define MQ_TILE_ENTRIES 2560 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
 #define MQ_REG_ROW 128        /* tile rows longer than this (medium rows) are
                                  solved by the warp-per-row path          */
+#define MQ_WS_SLOTS 16        /* working-set slots per row (screened solve)  */
 
 /* Read-only market description (device pointers, borrowed).  Arrays marked
  * [pad] must have 16 readable bytes past their last element (TMA bulk copies
@@ -92,8 +93,9 @@ typedef struct mq_state {
     double *cs;       /* [m]   colsum(x^k)                                     */
     double *cs_prev;  /* [m]   colsum(x^{k-1})                                 */
     double *csbar;    /* [m]   colsum(xbar)                                    */
-    int32_t *blk_done;/* [3] the primal kernels' dynamic work counters (tiles,
-                         long rows, medium rows)                               */
+    int32_t *blk_done;/* [8] the primal kernels' dynamic work counters (tiles,
+                         long rows, medium rows, full-solve list length, its
+                         claim counter), zeroed by mq_primal_step            */
     const double *steps; /* [2] tau, sigma (device-resident: one graph serves
                             every step size)                                   */
     int64_t *navg;    /* [1]  inner iterations since the last restart          */
@@ -111,6 +113,28 @@ typedef struct mq_state {
        whenever it writes x, xbar or navg itself.                            */
     uint8_t *xflag;   /* [nnz] [pad]                                          */
     double *xsum;     /* [nnz]                                                */
+    /* Working set of the screened row solve; ws_len == NULL
+       selects the unscreened tile kernel.  For a zero entry x_ij = 0, the
+       prox keeps it at zero iff p_j s_i >= w_i u_ij (s_i = the row's root),
+       so a row is solved over its working set only — nonzero and "near"
+       entries, at most MQ_WS_SLOTS, held in slots — and the result is the
+       full row's when the certificate
+           theta_i (1 - D / P_i) s >= w_i (1 + 1e-12)
+       holds, theta_i = min p_j / u_ij and P_i = min p_j over the screened
+       entries at the working set's last rebuild and D the accumulated price
+       decrease since (drift); otherwise (and when ws_len < 0) the row is
+       solved in full and its working set rebuilt.  ws_len[i]: slots in use
+       (>= 0); -1 no valid working set; -2 larger than MQ_WS_SLOTS (solved in
+       full every iteration); -3 not a tile row (medium / long kernels).  The
+       host writes -1 (keeping -3) whenever it writes x or p itself.       */
+    int32_t *ws_len;  /* [n]                                                  */
+    double *ws_cert;  /* [4n] theta, P, C at the rebuild, unused             */
+    double *ws_ux;    /* [2 n MQ_WS_SLOTS] (u, x) per slot, ascending entry  */
+    int32_t *ws_cp;   /* [2 n MQ_WS_SLOTS] (column, entry offset in the row) */
+    int32_t *ws_list; /* [n] rows solved in full this iteration               */
+    double *drift;    /* [2] C = accumulated bound on the largest price
+                         decrease (rounded up), this iteration's decrease
+                         (bit pattern, order-free max)                      */
 } mq_state;
 
 /* Mutable iterate of the lifted PDHG path (algo="pdhg", kernels.py:146-197):
@@ -298,6 +322,8 @@ const char *mq_last_error(void);
 int mq_abi_version(void);
 /* 1 if the build sums columns in fixed point (state.bucket = m u64) */
 int mq_fixed_colsum(void);
+/* working-set slots per row of this build (MQ_WS_SLOTS) */
+int mq_ws_slots(void);
 /* 1 if the build keeps the sparse iterate (xflag / xsum) */
 int mq_x_sparse(void);
 /* sparse iterate: xbar = xsum / navg (call after mq_chunk_end) */

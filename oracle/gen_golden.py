@@ -476,10 +476,36 @@ def c2_lockstep():
         out[f"{tag}_x_sample"] = x[:: 997]
         out[f"{tag}_x_sha"] = hashlib.sha256(x.tobytes()).hexdigest()
         out[f"{tag}_xbar_sha"] = hashlib.sha256(xbar.tobytes()).hexdigest()
-        out[f"{tag}_ux"] = me.kkt.SparseMatrix.row_sums(inst.utilities, inst.utilities.values * x)
+        out[f"{tag}_ux"] = inst.utilities.row_sums(inst.utilities.values * x)
     out["tau"] = tau
     out["fingerprint"] = me.instance_fingerprint(inst)
     save("c2_lockstep.npz", **out)
+
+
+def c2_solve():
+    """BASELINE config 2 solved to 1e-4 by the reference at subproblem_tol=0
+    (the default 1e-10 bracket crashes at iteration 41).
+    ~2.5 h on 8 cores; the allocation (1e7 entries) is kept as a checksum, a
+    strided sample and the per-buyer utilities."""
+    t = time.time()
+    inst = me.generate_fisher(me.GeneratorConfig(n=100_000, m=10_000, sparsity_u=0.01, seed=0))
+    print(f"  C2 generated in {time.time() - t:.1f}s, nnz={inst.utilities.nnz}", flush=True)
+    import logging
+    logging.basicConfig(level=logging.INFO)
+    cfg = me.SolveConfig(tol=1e-4, subproblem_tol=0.0)
+    t = time.time()
+    rep = me.run_solve(inst, cfg, "pdhcg")
+    t_ref = time.time() - t
+    obj = me.kkt.eg_objective(inst, rep.allocation)
+    d = report_arrays(rep, with_alloc=False)
+    d["allocation_sha"] = hashlib.sha256(rep.allocation.tobytes()).hexdigest()
+    d["allocation_sample"] = rep.allocation[::997]
+    d["allocation_sum"] = np.array([rep.allocation.sum(), (rep.allocation ** 2).sum()])
+    save("solve_c2_tol0.npz", **d, objective=obj, tol=cfg.tol, subtol=cfg.subproblem_tol,
+         sections=cfg.sections, max_iters=cfg.max_iters, ref_seconds=t_ref,
+         threads=os.cpu_count())
+    print(f"  C2 tol0: {rep.status} iters={rep.inner_iterations} restarts={rep.restarts} "
+          f"obj={obj!r} ref {t_ref:.1f}s", flush=True)
 
 
 def main():
@@ -493,11 +519,11 @@ def main():
              "pdhg": pdhg_cases, "theory": theory_case, "fileio": fileio_case,
              "bigsolve": big_solve_cases,
              "resid": resid_cases, "exchange": exchange_case,
-             "gen": lambda: gen_fingerprints(a.big), "c2": c2_lockstep}
+             "gen": lambda: gen_fingerprints(a.big), "c2": c2_lockstep, "c2solve": c2_solve}
     for k, fn in steps.items():
         if a.only and k not in a.only.split(","):
             continue
-        if k in ("c2", "bigsolve") and not a.big:
+        if k in ("c2", "bigsolve", "c2solve") and not a.big:
             continue
         print(f"[{k}]")
         fn()

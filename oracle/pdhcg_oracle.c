@@ -30,6 +30,7 @@
 #include <string.h>
 #include <pthread.h>
 #include <stdatomic.h>
+#include <stdlib.h>
 
 #define ORC_MAX_ROW_PASSES 200          /* kernels.py:16 */
 #define ORC_REL_WIDTH_FLOOR 4e-16       /* kernels.py:19 */
@@ -282,4 +283,127 @@ int orc_set_threads(int nthreads)
     if (nthreads > 0)
         g_threads = nthreads > 256 ? 256 : nthreads;
     return g_threads;
+}
+
+/* ---- setup helpers for markets numpy cannot set up in reasonable time
+ * (bench.py's CPU legs at config 4, nnz ~1e9); same arithmetic as the
+ * reference's numpy setup. ---- */
+typedef struct {
+    const int64_t *indptr;
+    const double *val;
+    double *out, *scales;
+} orc_norm_ctx;
+
+/* normalize (instance.py:118-138): scale_i = max_j u_ij, u_ij / scale_i */
+static void orc_norm_rows(void *vc, int64_t lo, int64_t hi, int64_t *acc)
+{
+    orc_norm_ctx *C = (orc_norm_ctx *)vc;
+    for (int64_t i = lo; i < hi; ++i) {
+        double mx = 0.0;
+        for (int64_t t = C->indptr[i]; t < C->indptr[i + 1]; ++t)
+            if (C->val[t] > mx)
+                mx = C->val[t];
+        C->scales[i] = mx;
+        if (mx == 0.0)
+            acc[1] += 1;
+        for (int64_t t = C->indptr[i]; t < C->indptr[i + 1]; ++t)
+            C->out[t] = C->val[t] / mx;
+    }
+}
+
+/* returns the number of rows without a positive value (the reference raises) */
+int64_t orc_normalize(int64_t n, const int64_t *indptr, const double *val, double *out,
+                      double *scales)
+{
+    orc_norm_ctx C = {indptr, val, out, scales};
+    int64_t acc[2];
+    orc_parallel_for(n, 4096, orc_norm_rows, &C, acc);
+    return acc[1];
+}
+
+/* Stable transpose schedule (sparse.py:130-145: argsort(col, stable)):
+ * counting sort, each thread scattering a contiguous entry range after the
+ * ranges before it, so equal columns keep ascending storage order. */
+typedef struct {
+    const int32_t *col;
+    int64_t nnz, m, nparts;
+    int64_t *cnt; /* nparts x m */
+    int32_t *tperm;
+} orc_tr_ctx;
+
+static void orc_tr_count(void *vc, int64_t lo, int64_t hi, int64_t *acc)
+{
+    orc_tr_ctx *C = (orc_tr_ctx *)vc;
+    (void)acc;
+    for (int64_t q = lo; q < hi; ++q) {
+        int64_t a = C->nnz * q / C->nparts, b = C->nnz * (q + 1) / C->nparts;
+        int64_t *c = C->cnt + q * C->m;
+        for (int64_t t = a; t < b; ++t)
+            c[C->col[t]]++;
+    }
+}
+
+static void orc_tr_scatter(void *vc, int64_t lo, int64_t hi, int64_t *acc)
+{
+    orc_tr_ctx *C = (orc_tr_ctx *)vc;
+    (void)acc;
+    for (int64_t q = lo; q < hi; ++q) {
+        int64_t a = C->nnz * q / C->nparts, b = C->nnz * (q + 1) / C->nparts;
+        int64_t *c = C->cnt + q * C->m;
+        for (int64_t t = a; t < b; ++t)
+            C->tperm[c[C->col[t]]++] = (int32_t)t;
+    }
+}
+
+/* tperm [nnz] int32, tindptr [m+1] int64; returns -1 when scratch fails */
+int orc_transpose(int64_t m, int64_t nnz, const int32_t *col, int32_t *tperm, int64_t *tindptr)
+{
+    int64_t nparts = g_threads * 4;
+    if (nparts < 1)
+        nparts = 1;
+    int64_t *cnt = (int64_t *)calloc((size_t)(nparts * m), sizeof(int64_t));
+    if (!cnt)
+        return -1;
+    orc_tr_ctx C = {col, nnz, m, nparts, cnt, tperm};
+    orc_parallel_for(nparts, 1, orc_tr_count, &C, NULL);
+    int64_t run = 0;
+    for (int64_t j = 0; j < m; ++j) {
+        tindptr[j] = run;
+        for (int64_t q = 0; q < nparts; ++q) {
+            int64_t c = cnt[q * m + j];
+            cnt[q * m + j] = run;
+            run += c;
+        }
+    }
+    tindptr[m] = run;
+    orc_parallel_for(nparts, 1, orc_tr_scatter, &C, NULL);
+    free(cnt);
+    return 0;
+}
+
+typedef struct {
+    const int32_t *tperm;
+    const int64_t *tindptr;
+    const double *v;
+    double *out;
+} orc_cs_ctx;
+
+static void orc_cs_cols(void *vc, int64_t lo, int64_t hi, int64_t *acc)
+{
+    orc_cs_ctx *C = (orc_cs_ctx *)vc;
+    (void)acc;
+    for (int64_t j = lo; j < hi; ++j) {
+        double a = 0.0;
+        for (int64_t t = C->tindptr[j]; t < C->tindptr[j + 1]; ++t)
+            a += C->v[C->tperm[t]];
+        C->out[j] = a;
+    }
+}
+
+/* column sums in ascending storage order (np.bincount(col, weights=v)) */
+void orc_colsums(int64_t m, const int32_t *tperm, const int64_t *tindptr, const double *v,
+                 double *out)
+{
+    orc_cs_ctx C = {tperm, tindptr, v, out};
+    orc_parallel_for(m, 64, orc_cs_cols, &C, NULL);
 }

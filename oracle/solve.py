@@ -59,6 +59,12 @@ def _load():
             lib.orc_row_root.argtypes = [i64, i64, P, P, f64, f64, cint, f64, P]
             lib.orc_set_threads.restype = cint
             lib.orc_set_threads.argtypes = [cint]
+            lib.orc_normalize.restype = i64
+            lib.orc_normalize.argtypes = [i64, P, P, P, P]
+            lib.orc_transpose.restype = cint
+            lib.orc_transpose.argtypes = [i64, i64, P, P, P]
+            lib.orc_colsums.restype = None
+            lib.orc_colsums.argtypes = [i64, P, P, P, P]
             _lib = lib
     return _lib
 
@@ -112,6 +118,108 @@ def row_root(uval, cbuf, tw, s0, sections=32, tol=1e-10):
     s = lib.orc_row_root(0, len(uval), _ptr(uval), _ptr(cbuf), float(tw), float(s0),
                          int(sections), float(tol), ctypes.byref(passes))
     return s, int(passes.value)
+
+
+# ------------------------------------------------- large-market setup (C)
+
+def normalize_rows(indptr, val):
+    """(val / row max, row max) as instance.py:118-138 computes them, in C
+    (the numpy path needs nnz-sized int64 temporaries at config 4)."""
+    lib = _load()
+    indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+    val = np.ascontiguousarray(val, dtype=np.float64)
+    n = len(indptr) - 1
+    out = np.empty_like(val)
+    scales = np.empty(n)
+    if lib.orc_normalize(n, _ptr(indptr), _ptr(val), _ptr(out), _ptr(scales)):
+        raise ValueError("cannot normalize: some buyer values no good")
+    return out, scales
+
+
+def transpose_int32(col, m):
+    """(tperm int32, tindptr int64) = sparse.py:130-145's stable argsort by
+    column, as a parallel stable counting sort."""
+    lib = _load()
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    tperm = np.empty(len(col), dtype=np.int32)
+    tindptr = np.empty(m + 1, dtype=np.int64)
+    if lib.orc_transpose(m, len(col), _ptr(col), _ptr(tperm), _ptr(tindptr)):
+        raise MemoryError("orc_transpose scratch")
+    return tperm, tindptr
+
+
+def column_sums_sched(tperm, tindptr, v):
+    """np.bincount(col, weights=v) through the transpose schedule."""
+    out = np.empty(len(tindptr) - 1)
+    _load().orc_colsums(len(out), _ptr(tperm), _ptr(tindptr), _ptr(v), _ptr(out))
+    return out
+
+
+def selector_norm_from_counts(counts, iters=50):
+    """The reference's op-norm power iteration (sparse.py:213-233) run on the
+    column counts (its iterate is constant within a column): equal to
+    op_norm_estimate of the selector to ~1e-15 at O(m) cost."""
+    c = np.asarray(counts, dtype=np.float64)
+    nnz = float(c.sum())
+    if nnz == 0 or len(c) == 0:
+        return 0.0
+    v = np.full(len(c), 1.0 / np.sqrt(nnz))
+    sig = 0.0
+    for _ in range(iters):
+        wv = c * v
+        sig = float(np.sqrt(np.dot(c, wv * wv)))
+        if sig == 0.0:
+            return 0.0
+        v = wv / sig
+    return float(np.sqrt(sig))
+
+
+class ChunkRun:
+    """The reference's compact iterate on a large market, set up the way
+    _CompactRun (driver.py:94-132) does it: normalized utilities, transpose
+    schedule, initial state x = 1/colcount, p = sum(w)/m (pdhcg.py:66-72),
+    L from the column counts, omega_0 from the residual norms and the first
+    restart window's steps tau = eta/omega, sigma = eta*omega with
+    eta = 0.9 / L (adaptive.py).  `step(k)` runs k iterations of the
+    restated kernels.pdhcg_chunk and returns their pass counts."""
+
+    def __init__(self, row_ptr, col, val, w, m, sections=32, subtol=1e-10):
+        self.indptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        self.col = np.ascontiguousarray(col, dtype=np.int32)
+        self.w = np.ascontiguousarray(w, dtype=np.float64)
+        self.n, self.m = len(self.indptr) - 1, int(m)
+        self.val, _ = normalize_rows(self.indptr, val)
+        self.tperm, self.tindptr = transpose_int32(self.col, self.m)
+        counts = np.diff(self.tindptr).astype(np.float64)
+        self.x = (1.0 / counts)[self.col]
+        self.p = np.full(self.m, float(np.sum(self.w)) / self.m)
+        self.x_prev, self.xbar, self.pbar = self.x.copy(), self.x.copy(), self.p.copy()
+        self.cbuf = np.empty_like(self.x)
+        self.navg = 0
+        self.L = max(selector_norm_from_counts(counts), np.finfo(float).tiny)
+        primal = float(np.linalg.norm(column_sums_sched(self.tperm, self.tindptr, self.x) - 1.0))
+        if primal > 1e-8:  # driver.py:123-132 needs the dual residual too
+            ux = np.add.reduceat(self.val * self.x, self.indptr[:-1])
+            uy = self.val * np.repeat(self.w / ux, np.diff(self.indptr))
+            best = np.full(self.m, -np.inf)
+            np.maximum.at(best, self.col, uy)
+            dual = float(np.linalg.norm(np.minimum(self.p - best, 0.0)))
+            self.omega0 = max(1.0, dual / primal) if dual > 1e-8 else 1.0
+        else:
+            self.omega0 = 1.0
+        eta = 0.9 / self.L
+        self.tau, self.sigma = eta / self.omega0, eta * self.omega0
+        self.sections, self.subtol = sections, subtol
+
+    def step(self, iters=1):
+        passes = np.zeros(iters, dtype=np.int64)
+        self.navg, faults = pdhcg_chunk(self.indptr, self.col, self.val, self.tperm,
+                                        self.tindptr, self.w, self.x, self.x_prev, self.p,
+                                        self.xbar, self.pbar, self.navg, self.tau, self.sigma,
+                                        self.sections, self.subtol, iters, self.cbuf, passes)
+        if faults:
+            raise RuntimeError(f"{faults} row subproblems exceeded {MAX_ROW_PASSES} passes")
+        return passes
 
 
 # ---------------------------------------------------------------- market data

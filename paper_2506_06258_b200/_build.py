@@ -25,7 +25,7 @@ SOURCES = {
     "abi.cu": [],
     "fast.cu": [],
     "reduce.cu": [],
-    "generate.cu": [],
+    "generate.cu": ["--fmad=false"],
     "lifted.cu": [],
     "theory.cu": [],
     "ksection.cu": ["--fmad=false"],

@@ -18,7 +18,8 @@ LONG_ROW = int(os.environ.get("MQ_LONG_ROW", "1024"))  # MQ_LONG_ROW (tuning ove
 REG_ROW = 128         # MQ_REG_ROW
 TILE_ROWS = 256       # MQ_TILE_ROWS
 PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
-ABI_VERSION = 7
+ABI_VERSION = 8
+WS_SLOTS = 16          # MQ_WS_SLOTS
 
 _lock = threading.Lock()
 _lib = None
@@ -51,7 +52,8 @@ class MqState(ctypes.Structure):
     _fields_ = [("x", P), ("xbar", P), ("p", P), ("pbar", P), ("cs", P), ("cs_prev", P),
                 ("csbar", P), ("blk_done", P), ("steps", P), ("navg", P),
                 ("pass_out", P), ("faults", P), ("bucket", P), ("srow", P),
-                ("xflag", P), ("xsum", P)]
+                ("xflag", P), ("xsum", P), ("ws_len", P), ("ws_cert", P), ("ws_ux", P),
+                ("ws_cp", P), ("ws_list", P), ("drift", P)]
 
 
 PM = ctypes.POINTER(MqMarket)
@@ -93,6 +95,7 @@ _SIGS = {
     "mq_abi_version": (CINT, []),
     "mq_fixed_colsum": (CINT, []),
     "mq_x_sparse": (CINT, []),
+    "mq_ws_slots": (CINT, []),
     "mq_avg_materialize": (CINT, [PM, PS, P]),
     "mq_pdhg_step": (CINT, [PM, PL, CINT, P]),
     "mq_pdhg_colsum_only": (CINT, [PM, PL, CINT, P]),

@@ -37,6 +37,8 @@
 // Variants measured along the way (dense iterate with gathered / bucketed /
 // scattered column sums, gather warps, software pipelining, ...) are listed
 // with their numbers in DESIGN.md §11.
+#include <math_constants.h>
+
 #include "mq_common.cuh"
 
 // ---- compile-time configuration (tuning variants override with -D) ----
@@ -199,8 +201,8 @@ __device__ __forceinline__ void fixed_colsum_add(const mq_market &mk, const mq_s
         asm volatile("red.global.add.u64 [%0], %1;" ::"l"(reinterpret_cast<unsigned long long *>(
                          st.bucket) + j),
                      "l"(__double2ull_rn(xe * mk.cs_scale)));
-    } else {
-        atomicAdd(reinterpret_cast<unsigned long long *>(st.faults), 1ull);
+    } else {  // out of the fixed-point range: faults[1] (engine raises FixedPointRangeError)
+        atomicAdd(reinterpret_cast<unsigned long long *>(st.faults) + 1, 1ull);
     }
 }
 
@@ -218,20 +220,29 @@ __device__ __forceinline__ void put_x(const mq_market &mk, const mq_state &st, i
 }
 
 // ------------------------------------------------------------ price step
+// drift (may be NULL): drift[1] = max_j (p_j^old - p_j^new)_+ rounded up, an
+// order-free max on the bit patterns (the working set's certificate)
 __global__ void dual_kernel(int64_t m, double *__restrict__ p, double *__restrict__ pbar,
                             double *__restrict__ cs, double *__restrict__ cs_prev,
                             const double *__restrict__ steps, const int64_t *__restrict__ navg,
-                            int it) {
+                            int it, double *__restrict__ drift) {
     const double sigma = steps[1];
     const Avg w = avg_weights(navg, it);
+    double dec = 0.0;
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
          j += (int64_t)gridDim.x * blockDim.x) {
         const double c = cs[j];
         const double acc = 2.0 * c - cs_prev[j];  // colsum(2 x^k - x^{k-1})
-        const double pj = p[j] + sigma * (acc - 1.0);
+        const double pold = p[j];
+        const double pj = pold + sigma * (acc - 1.0);
         p[j] = pj;
         pbar[j] = w.wold * pbar[j] + w.wnew * pj;
         cs_prev[j] = c;
+        dec = fmax(dec, __dsub_ru(pold, pj));
+    }
+    if (drift) {
+        dec = group_max<32>(dec);
+        if ((threadIdx.x & 31) == 0) atomic_max_nonneg(drift + 1, dec);
     }
 }
 
@@ -977,6 +988,283 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
         atomicAdd((unsigned long long *)st.faults, (unsigned long long)my_faults);
 }
 
+// ------------------------------------------------------------ working set
+// Safe screening of the row solve (include/market_eq_b200.h
+// mq_state.ws_*).  A zero entry stays zero through the prox iff
+// c s + tau w u <= 0 with c = -tau p, i.e. p s >= w u: inactive entries never
+// enter the root (masked) nor change.  A row whose zero entries satisfy that
+// with margin at the row's root can therefore be solved over the rest —
+// its working set: the nonzero entries plus the zero entries within a factor
+// MQ_WS_GAMMA of the threshold — and gives exactly the full row's active set,
+// root and allocation.  The certificate needs no look at the screened
+// entries: their prices have dropped by at most D (drift) since the working
+// set was built, so p_j s >= (p_j^ref - D) s >= theta (1 - D / P) s with
+// theta = min p^ref / u and P = min p^ref over them.  On C4 the working sets
+// hold ~6 % of the entries and the certificate holds for ~100 % of the rows
+// (tools/screen_stats.py): one price gather in ~16 instead of every entry's.
+#ifndef MQ_WS_GAMMA
+#define MQ_WS_GAMMA 1.05
+#endif
+#ifndef MQ_WS_MARGIN
+#define MQ_WS_MARGIN 1e-12
+#endif
+constexpr int kWsG = 8;                     // lanes per row: 4 rows per warp
+constexpr int kWsPer = MQ_WS_SLOTS / kWsG;  // slots per lane
+
+// Append `row` to this iteration's full-solve list (one lane per row pushes;
+// warp-aggregated).  The list order is irrelevant to the results: rows are
+// independent and the column sums are order-free.
+__device__ __forceinline__ void ws_push(const mq_state &st, bool push, int64_t row) {
+    const uint32_t b = __ballot_sync(MQ_FULL, push);
+    if (!b) return;
+    const int wl = threadIdx.x & 31;
+    const int leader = __ffs(b) - 1;
+    int base = 0;
+    if (wl == leader) base = atomicAdd(st.blk_done + 3, __popc(b));
+    base = __shfl_sync(MQ_FULL, base, leader);
+    if (push) st.ws_list[base + __popc(b & ((1u << wl) - 1u))] = (int32_t)row;
+}
+
+// price-decrease bound of this iteration: C + dec, rounded up (the value the
+// column-sum kernel stores as the next C)
+__device__ __forceinline__ double drift_now(const mq_state &st) {
+    return __dadd_ru(st.drift[0], st.drift[1]);
+}
+
+// Screened solve of every tile row with a working set (ws_len >= 0), 8 lanes
+// per row, slots in registers.  Rows without one, or whose certificate
+// fails, go to the full-solve list untouched.
+#ifndef MQ_WS_MINB
+#define MQ_WS_MINB 3  // resident 256-thread CTAs per SM of the screened solve
+#endif
+__global__ void __launch_bounds__(256, MQ_WS_MINB)
+ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
+    constexpr int G = kWsG, PER = kWsPer, K = MQ_WS_SLOTS, RPW = 32 / G;
+    const double tau = st.steps[0];
+    const double cnow = drift_now(st);
+    const int wl = threadIdx.x & 31, lane = wl & (G - 1), gsub = wl / G;
+    const uint32_t gmask = ((1u << G) - 1u) << (gsub * G);
+    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double2 *__restrict__ ux2 = reinterpret_cast<const double2 *>(st.ws_ux);
+    const int2 *__restrict__ cp2 = reinterpret_cast<const int2 *>(st.ws_cp);
+    int my_sweeps = 0;
+    for (int64_t q = warp0; q * RPW < mk.n; q += nwarps) {
+        const int64_t i = q * RPW + gsub;
+        const bool has = i < mk.n;
+        int h = has ? __ldcg(st.ws_len + i) : -3;
+        if (force_full && h != -3) h = -1;
+        ws_push(st, has && lane == 0 && (h == -1 || h == -2), i);
+        const bool act = has && h >= 0;
+        double u[PER], c[PER], xo[PER], pv[PER];
+        int jc[PER], pos[PER];
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+            const int slot = lane + e * G;
+            double2 a = make_double2(0.0, 0.0);
+            int2 b = make_int2(0, 0);
+            if (act && slot < h) {
+                a = __ldcg(ux2 + i * K + slot);
+                b = __ldcg(cp2 + i * K + slot);
+            }
+            u[e] = a.x;
+            xo[e] = a.y;
+            jc[e] = b.x;
+            pos[e] = b.y;
+        }
+        double w = 0.0, s0 = 0.0;
+        double2 cert01 = make_double2(0.0, 0.0);
+        double cref = 0.0;
+        if (act) {
+            w = __ldg(mk.w + i);
+            s0 = st.srow[i];
+            cert01 = __ldcg(reinterpret_cast<const double2 *>(st.ws_cert) + 2 * i);
+            cref = __ldcg(st.ws_cert + 4 * i + 2);
+        }
+#pragma unroll
+        for (int e = 0; e < PER; ++e) pv[e] = (act && lane + e * G < h) ? __ldg(st.p + jc[e]) : 0.0;
+        const double tw = tau * w;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) c[e] = xo[e] - tau * pv[e];
+        int nsw = 0;
+        bool ok = true;
+        const double s = row_root_warm<G, PER>(c, u, tw, s0, act, gmask, &nsw, &ok);
+        bool pass = false;
+        if (act && ok) {
+            // directed rounding: lhs rounded down, rhs up (a sound test)
+            const double D = fmax(__dsub_ru(cnow, cref), 0.0);
+            const double f = __dadd_rd(1.0, -__ddiv_ru(D, cert01.y));
+            const double lhs = __dmul_rd(__dmul_rd(cert01.x, f), s);
+            pass = f > 0.0 && lhs >= __dmul_ru(w, 1.0 + MQ_WS_MARGIN);
+        }
+        ws_push(st, act && lane == 0 && !pass, i);
+        if (pass) {  // uniform over the row's lanes
+            const int64_t e0 = __ldg(mk.row_ptr + i);
+            const double inv_s = 1.0 / s;
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int slot = lane + e * G;
+                if (slot < h) {
+                    const double xn = fmax(c[e] + tw * u[e] * inv_s, 0.0);
+                    const int64_t g = e0 + pos[e];
+                    if (xn != xo[e]) {
+                        st.ws_ux[2 * (i * K + slot) + 1] = xn;
+                        st.x[g] = xn;
+                        if ((xn > 0.0) != (xo[e] > 0.0)) st_flag(st.xflag + g, xn > 0.0);
+                    }
+                    if (xn > 0.0) {
+                        red_add_f64(st.xsum + g, xn);
+                        fixed_colsum_add(mk, st, jc[e], xn);
+                    }
+                }
+            }
+            if (lane == 0) {
+                st.srow[i] = s;
+                my_sweeps += nsw;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_sweeps += __shfl_xor_sync(MQ_FULL, my_sweeps, o);
+    if (wl == 0 && my_sweeps)
+        atomicAdd((unsigned long long *)(st.pass_out + it), (unsigned long long)my_sweeps);
+}
+
+// Full solve of the listed rows (no working set, a failed certificate, more
+// than MQ_WS_SLOTS working entries, or x_prev_out requested), 16 lanes per row,
+// the row (<= MQ_REG_ROW entries) in registers, then the working set rebuilt:
+// slots in ascending entry order, theta / P over the screened entries, C.
+__global__ void __launch_bounds__(256)
+ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
+    constexpr int G = 16, RP = MQ_REG_PER, K = MQ_WS_SLOTS;
+    const double tau = st.steps[0];
+    const double cnow = drift_now(st);
+    const int wl = threadIdx.x & 31, lane = wl & (G - 1), gsub = wl / G;
+    const uint32_t gmask = ((1u << G) - 1u) << (gsub * G);
+    const int count = *(volatile int32_t *)(st.blk_done + 3);
+    double2 *__restrict__ ux2 = reinterpret_cast<double2 *>(st.ws_ux);
+    int2 *__restrict__ cp2 = reinterpret_cast<int2 *>(st.ws_cp);
+    int my_sweeps = 0, my_faults = 0;
+    for (;;) {
+        int rb = 0;
+        if (wl == 0) rb = atomicAdd(st.blk_done + 4, 2);
+        rb = __shfl_sync(MQ_FULL, rb, 0);
+        if (rb >= count) break;  // warp-uniform
+        const int r = rb + gsub;
+        const bool has = r < count;
+        const int64_t i = has ? st.ws_list[r] : 0;
+        int64_t a = 0;
+        int len = 0;
+        double w = 0.0, s0 = 0.0;
+        int hold = -3;
+        if (has) {
+            a = __ldg(mk.row_ptr + i);
+            len = (int)(__ldg(mk.row_ptr + i + 1) - a);
+            w = __ldg(mk.w + i);
+            s0 = st.srow[i];
+            hold = __ldcg(st.ws_len + i);
+        }
+        double c[RP], u[RP], pv[RP], xv[RP];
+        int jc[RP];
+        uint32_t fb = 0;
+#pragma unroll
+        for (int e = 0; e < RP; ++e) {
+            const int t = lane + e * G;
+            const bool in = t < len;
+            jc[e] = in ? __ldg(mk.col + a + t) : 0;
+            u[e] = in ? __ldg(mk.u + a + t) : 0.0;
+            if (in && __ldcg(st.xflag + a + t)) fb |= 1u << e;
+        }
+#pragma unroll
+        for (int e = 0; e < RP; ++e) {
+            const int t = lane + e * G;
+            pv[e] = t < len ? __ldg(st.p + jc[e]) : 0.0;
+            xv[e] = ((fb >> e) & 1u) ? __ldcg(st.x + a + t) : 0.0;
+        }
+        const double tw = tau * w;
+#pragma unroll
+        for (int e = 0; e < RP; ++e) {
+            c[e] = xv[e] - tau * pv[e];
+            const int t = lane + e * G;
+            if (x_prev_out && t < len) x_prev_out[a + t] = xv[e];
+        }
+        int nsw = 0;
+        bool ok = true;
+        const double s = row_root_warm<G, RP>(c, u, tw, s0, has, gmask, &nsw, &ok);
+        const double inv_s = 1.0 / s;
+        double xn[RP];
+#pragma unroll
+        for (int e = 0; e < RP; ++e) {
+            const int t = lane + e * G;
+            xn[e] = t < len ? fmax(c[e] + tw * u[e] * inv_s, 0.0) : 0.0;
+            if (t < len) {
+                const bool nz = xn[e] > 0.0, was = (fb >> e) & 1u;
+                const int64_t g = a + t;
+                if (nz != was) st_flag(st.xflag + g, nz);
+                if (nz || was) st.x[g] = xn[e];
+                if (nz) {
+                    red_add_f64(st.xsum + g, xn[e]);
+                    fixed_colsum_add(mk, st, jc[e], xn[e]);
+                }
+            }
+        }
+        // working set: nonzero entries and zero entries near the threshold
+        // (p s < gamma w u), ranked by entry position t = lane + 16 e
+        const bool build = has && hold != -3;
+        const double gw = MQ_WS_GAMMA * w;
+        int before = 0, rank[RP];
+        uint32_t hot = 0;
+        double th = CUDART_INF, pm = CUDART_INF;
+#pragma unroll
+        for (int e = 0; e < RP; ++e) {
+            const int t = lane + e * G;
+            const bool in = build && t < len;
+            const bool hb = in && (xn[e] > 0.0 || pv[e] * s < gw * u[e]);
+            if (hb) hot |= 1u << e;
+            if (in && !hb) {
+                th = fmin(th, __ddiv_rd(pv[e], u[e]));
+                pm = fmin(pm, pv[e]);
+            }
+            const uint32_t bal = (__ballot_sync(MQ_FULL, hb) >> (gsub * G)) & ((1u << G) - 1u);
+            rank[e] = before + __popc(bal & ((1u << lane) - 1u));
+            before += __popc(bal);
+        }
+        th = group_min<G>(th);
+        pm = group_min<G>(pm);
+        if (build) {
+            if (before <= K) {
+#pragma unroll
+                for (int e = 0; e < RP; ++e) {
+                    if ((hot >> e) & 1u) {
+                        ux2[i * K + rank[e]] = make_double2(u[e], xn[e]);
+                        cp2[i * K + rank[e]] = make_int2(jc[e], lane + e * G);
+                    }
+                }
+                if (lane == 0) {
+                    reinterpret_cast<double2 *>(st.ws_cert)[2 * i] = make_double2(th, pm);
+                    st.ws_cert[4 * i + 2] = cnow;
+                    st.ws_len[i] = before;
+                }
+            } else if (lane == 0) {
+                st.ws_len[i] = -2;
+            }
+        }
+        if (has && lane == 0) {
+            st.srow[i] = s;
+            my_sweeps += nsw;
+            if (!ok) ++my_faults;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        my_sweeps += __shfl_xor_sync(MQ_FULL, my_sweeps, o);
+        my_faults += __shfl_xor_sync(MQ_FULL, my_faults, o);
+    }
+    if (wl == 0 && my_sweeps)
+        atomicAdd((unsigned long long *)(st.pass_out + it), (unsigned long long)my_sweeps);
+    if (wl == 0 && my_faults) atomicAdd((unsigned long long *)st.faults, (unsigned long long)my_faults);
+}
+
 // ------------------------------------------------------------ column sums
 // Deterministic fp64 column sums over the blocked schedule (residual checks,
 // restarts: the reference's column_sums order): one thread per good walking
@@ -1008,8 +1296,14 @@ colsum_blocks_kernel(int64_t m, const int32_t *__restrict__ bptr, const int32_t 
 // iteration
 __global__ void cs_from_fixed_kernel(int64_t m, unsigned long long *__restrict__ fix,
                                      double *__restrict__ cs, double *__restrict__ csbar,
-                                     const int64_t *__restrict__ navg, int it, double inv_scale) {
+                                     const int64_t *__restrict__ navg, int it, double inv_scale,
+                                     double *__restrict__ drift) {
     const Avg av = avg_weights(navg, it);
+    if (drift && blockIdx.x == 0 && threadIdx.x == 0) {
+        // the primal kernels' C + dec, stored: the price-decrease bound so far
+        drift[0] = __dadd_ru(drift[0], drift[1]);
+        drift[1] = 0.0;
+    }
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
          j += (int64_t)gridDim.x * blockDim.x) {
         const double c = (double)fix[j] * inv_scale;  // exact for sums < 2^53 units
@@ -1064,11 +1358,16 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
         if (e != cudaSuccess) return set_error(e, "mq_primal_step: smem attribute");
         configured = true;
     }
-    // every dynamic work counter (tiles, long rows, medium rows) restarts at 0
-    cudaMemsetAsync(st->blk_done, 0, 3 * sizeof(int32_t), s);
-    if (mk->ntiles > 0)  // the dynamic tile counter lives in blk_done[0]
+    // every dynamic work counter (tiles, long rows, medium rows, full-solve
+    // list and its claims) restarts at 0
+    cudaMemsetAsync(st->blk_done, 0, 5 * sizeof(int32_t), s);
+    if (st->ws_len) {  // screened solve over working sets, then the full-solve list
+        ws_kernel<<<sm_count() * MQ_WS_MINB, 256, 0, s>>>(*mk, *st, it, xprev != nullptr);
+        ws_full_kernel<<<sm_count() * 3, 256, 0, s>>>(*mk, *st, it, xprev);
+    } else if (mk->ntiles > 0) {  // the dynamic tile counter lives in blk_done[0]
         kern<<<mk->prim_grid, (MQ_NSW + 1) * 32, kPrimalSmem, s>>>(*mk, *st, it, xprev, 0,
                                                                    mk->ntiles, st->blk_done);
+    }
     if (mk->nlong > 0) {
         using LS = LongSmem<MQ_LONG_THREADS, MQ_LONG_CAP>;
         auto lk = primal_long_kernel<MQ_LONG_THREADS, MQ_LONG_CAP>;
@@ -1092,15 +1391,16 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
 
 // shared with the lifted PDHG step (lifted.cu)
 int launch_dual(const mq_market *mk, double *p, double *pbar, double *cs, double *cs_prev,
-                const double *steps, const int64_t *navg, int it, cudaStream_t s) {
+                const double *steps, const int64_t *navg, int it, cudaStream_t s,
+                double *drift) {
     dual_kernel<<<grid_for(mk->m, 256, sm_count() * 8), 256, 0, s>>>(mk->m, p, pbar, cs, cs_prev,
-                                                                     steps, navg, it);
+                                                                     steps, navg, it, drift);
     return check_launch("mq_dual_step");
 }
 int launch_cs_from_fixed(const mq_market *mk, unsigned long long *fix, double *cs, double *csbar,
-                         const int64_t *navg, int it, cudaStream_t s) {
+                         const int64_t *navg, int it, cudaStream_t s, double *drift) {
     cs_from_fixed_kernel<<<grid_for(mk->m, 256, sm_count() * 8), 256, 0, s>>>(
-        mk->m, fix, cs, csbar, navg, it, 1.0 / mk->cs_scale);
+        mk->m, fix, cs, csbar, navg, it, 1.0 / mk->cs_scale, drift);
     return check_launch("mq_colsum_step");
 }
 
@@ -1112,7 +1412,7 @@ extern "C" {
 
 int mq_dual_step(const mq_market *mk, const mq_state *st, int it, void *stream) {
     return launch_dual(mk, st->p, st->pbar, st->cs, st->cs_prev, st->steps, st->navg, it,
-                       (cudaStream_t)stream);
+                       (cudaStream_t)stream, st->ws_len ? st->drift : nullptr);
 }
 
 int mq_primal_step(const mq_market *mk, const mq_state *st, int it, double *x_prev_out,
@@ -1124,7 +1424,7 @@ int mq_primal_step(const mq_market *mk, const mq_state *st, int it, double *x_pr
 int mq_colsum_step(const mq_market *mk, const mq_state *st, int it, int finalize, void *stream) {
     return launch_cs_from_fixed(mk, reinterpret_cast<unsigned long long *>(st->bucket), st->cs,
                                 finalize ? st->csbar : nullptr, st->navg, it,
-                                (cudaStream_t)stream);
+                                (cudaStream_t)stream, st->ws_len ? st->drift : nullptr);
 }
 
 int mq_colsum_finalize(const mq_market *mk, const mq_state *st, int it, void *stream) {
@@ -1173,6 +1473,7 @@ int mq_colsum_mode(void) { return 5; }   // fixed-point sparse column sums
 int mq_bucket_slots(void) { return 0; }  // no bucket mode in this build
 int mq_x_sparse(void) { return 1; }
 int mq_fixed_colsum(void) { return 1; }
+int mq_ws_slots(void) { return MQ_WS_SLOTS; }
 
 int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream) {
     const int grid = (int)((mk->m + 255) / 256);

@@ -5,10 +5,13 @@
 // markets) or d_i / m with a truncated power-law degree d_i (skewed markets).
 // Each row owns a Philox subsequence, so a row's content does not depend on
 // the launch configuration or on how rows are split across GPUs: rank r can
-// generate exactly its shard.
+// generate exactly its shard.  The transcendentals are the bit-specified
+// gm_log / gm_exp (mq_genmath.cuh), so oracle/market_gen.c regenerates any
+// market byte for byte on the host (the reference arm's instance, tests).
 #include <curand_kernel.h>
 
 #include "mq_common.cuh"
+#include "mq_genmath.cuh"
 
 namespace mq {
 
@@ -26,7 +29,8 @@ __device__ __forceinline__ double row_rate(const GenParams &g, int64_t row) {
     curandStatePhilox4_32_10_t st;
     curand_init(g.seed ^ 0x9e3779b97f4a7c15ull, (unsigned long long)row, 0, &st);
     const double u = curand_uniform_double(&st);  // (0, 1]
-    double d = g.dmin * pow(u, -1.0 / (g.alpha - 1.0));
+    const double k = -1.0 / (g.alpha - 1.0);
+    double d = __dmul_rn(g.dmin, gm_exp(__dmul_rn(k, gm_log(u))));
     if (d > (double)g.m) d = (double)g.m;
     return d / (double)g.m;
 }
@@ -43,18 +47,18 @@ __device__ int64_t walk_row(const GenParams &g, int64_t row, Emit emit) {
         for (int64_t j = 0; j < g.m; ++j) emit(j);
         return g.m;
     }
-    const double lq = log1p(-q);
+    const double lq = gm_log(__dadd_rn(1.0, -q));
     int64_t pos = -1;
     for (;;) {
         const double u = curand_uniform_double(&st);
-        const double skip = floor(log(u) / lq);
+        const double skip = floor(__ddiv_rn(gm_log(u), lq));
         if (skip >= (double)(g.m - 1 - pos)) break;
         pos += (int64_t)skip + 1;
         emit(pos);
         ++cnt;
     }
     if (cnt == 0) {  // repair: one uniformly placed entry (instance.py:165-194)
-        int64_t j = (int64_t)(curand_uniform_double(&st) * (double)g.m);
+        int64_t j = (int64_t)__dmul_rn(curand_uniform_double(&st), (double)g.m);
         if (j >= g.m) j = g.m - 1;
         emit(j);
         cnt = 1;

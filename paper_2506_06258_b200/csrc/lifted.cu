@@ -12,9 +12,11 @@
 namespace mq {
 
 int launch_dual(const mq_market *mk, double *p, double *pbar, double *cs, double *cs_prev,
-                const double *steps, const int64_t *navg, int it, cudaStream_t s);  // fast.cu
+                const double *steps, const int64_t *navg, int it, cudaStream_t s,
+                double *drift = nullptr);                                           // fast.cu
 int launch_cs_from_fixed(const mq_market *mk, unsigned long long *fix, double *cs, double *csbar,
-                         const int64_t *navg, int it, cudaStream_t s);              // fast.cu
+                         const int64_t *navg, int it, cudaStream_t s,
+                         double *drift = nullptr);                                  // fast.cu
 int sm_count_reduce();                                                              // reduce.cu
 
 namespace {

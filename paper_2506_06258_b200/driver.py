@@ -47,6 +47,7 @@ class SolveConfig:
     row_solver: str = "exact"          # "exact" (active-set closed form) or "ksection"
     device: object = None              # torch device / index; default current CUDA device
     use_graphs: bool = True            # CUDA-graph capture of chunks
+    working_set: bool = True           # screened row solves (exact)
 
     def __post_init__(self):
         if self.tol <= 0:
@@ -133,7 +134,7 @@ class DeviceSession:
             return
         self.engine = PdhcgEngine(self.dm, row_solver=cfg.row_solver, sections=cfg.sections,
                                   subproblem_tol=cfg.subproblem_tol, use_graphs=cfg.use_graphs,
-                                  group=group)
+                                  group=group, working_set=cfg.working_set)
         counts = self.engine._global_counts().cpu().numpy()
         self.op_norm = selector_norm_from_counts(counts)
 

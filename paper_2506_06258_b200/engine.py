@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .errors import SubproblemError
+from .errors import FixedPointRangeError, SubproblemError
 from .kkt import Residuals
 
 MAX_ROW_PASSES = 200  # kernels.py:16 (k-section fault threshold)
@@ -180,7 +180,7 @@ class NativeOps:
 
 class PdhcgEngine:
     def __init__(self, dm, row_solver="exact", sections=32, subproblem_tol=1e-10,
-                 use_graphs=True, group=None, ops_factory=None):
+                 use_graphs=True, group=None, ops_factory=None, working_set=True):
         if row_solver not in ("exact", "ksection"):
             raise ValueError("row_solver must be 'exact' or 'ksection'")
         self.dm = dm
@@ -217,8 +217,24 @@ class PdhcgEngine:
         # per-buyer utility of the last prox: the fused row solve's warm start
         self._srow_buf = torch.zeros(dm.n + nat.PAD, **f64)
         self.srow = self._srow_buf[:dm.n]
-        # the primal kernels' dynamic work counters (tiles, long rows, medium rows)
-        self.blk_done = torch.zeros(3, dtype=torch.int32, device=dev)
+        # the primal kernels' dynamic work counters (tiles, long rows, medium
+        # rows, full-solve list length and claims)
+        self.blk_done = torch.zeros(8, dtype=torch.int32, device=dev)
+        # working sets of the screened row solve: -3 marks the
+        # rows the medium / long kernels solve, -1 "no working set yet"
+        self.working_set = bool(working_set and self.sparse and hasattr(dm, "lib"))
+        if self.working_set:
+            K = nat.WS_SLOTS
+            lens = dm.row_ptr[1:] - dm.row_ptr[:-1]
+            self.ws_init = torch.where(lens > int(dm.lib.mq_reg_row()), -3, -1).to(torch.int32)
+            if dm.long_rows.numel():
+                self.ws_init[dm.long_rows.to(torch.int64)] = -3
+            self.ws_len = self.ws_init.clone()
+            self.ws_cert = torch.zeros(4 * max(1, dm.n), **f64)
+            self.ws_ux = torch.zeros(2 * K * max(1, dm.n), **f64)
+            self.ws_cp = torch.zeros(2 * K * max(1, dm.n), dtype=torch.int32, device=dev)
+            self.ws_list = torch.zeros(max(1, dm.n), dtype=torch.int32, device=dev)
+            self.drift = torch.zeros(2, **f64)
         # fixed-point column sums: m u64 accumulators, zero between iterations
         fixed = getattr(getattr(dm, "lib", None), "mq_fixed_colsum", None)
         self.fixed = bool(fixed is not None and fixed() == 1 and self.mode != "ksection")
@@ -234,7 +250,9 @@ class PdhcgEngine:
         self.resid_work = torch.zeros(2 * max(1, m), **f64)  # (p, column max) interleaved
         self.steps = torch.zeros(2, **f64)
         self.navg_dev = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.faults = torch.zeros(1, dtype=torch.int64, device=dev)
+        # [0] rows whose solve did not settle, [1] entries beyond the
+        # fixed-point column-sum range
+        self.faults = torch.zeros(2, dtype=torch.int64, device=dev)
         self.pass_buf = torch.zeros(1024, dtype=torch.int64, device=dev)
         nscr = int(dm.lib.mq_scratch_doubles()) if hasattr(dm, "lib") else 16
         self.scratch = torch.zeros(nscr, **f64)
@@ -266,6 +284,9 @@ class PdhcgEngine:
         for name in ("x", "xbar", "p", "pbar", "cs", "cs_prev", "csbar", "blk_done",
                      "steps", "faults", "srow", "bucket", "xflag", "xsum"):
             setattr(s, name, getattr(self, name).data_ptr())
+        if self.working_set:
+            for name in ("ws_len", "ws_cert", "ws_ux", "ws_cp", "ws_list", "drift"):
+                setattr(s, name, getattr(self, name).data_ptr())
         s.navg = self.navg_dev.data_ptr()
         s.pass_out = self.pass_buf.data_ptr()
         return s
@@ -285,8 +306,10 @@ class PdhcgEngine:
 
     # ------------------------------------------------------------ state
     def _sparse_sync(self):
-        """After the host wrote x, xbar or navg: every x may be nonzero, and
-        the running sum restarts from navg * xbar."""
+        """After the host wrote x, xbar or navg: every x may be nonzero, the
+        running sum restarts from navg * xbar and no working set is valid."""
+        if self.working_set:
+            self.ws_len.copy_(self.ws_init)
         if self.sparse:
             self.xflag.fill_(1)
             if self.navg:
@@ -373,6 +396,8 @@ class PdhcgEngine:
         self.cs.copy_(self.csbar)
         if self.sparse:
             self.xflag.fill_(1)
+        if self.working_set:
+            self.ws_len.copy_(self.ws_init)
 
     # ------------------------------------------------------------ chunks
     def run_chunk(self, iters):
@@ -392,8 +417,12 @@ class PdhcgEngine:
         self.navg += iters
         vals = torch.cat([self.pass_buf[:iters], self.faults]).cpu().numpy()
         if vals[-1]:
-            raise SubproblemError(f"{int(vals[-1])} row subproblems failed to converge")
-        return [int(v) for v in vals[:-1]]
+            raise FixedPointRangeError(
+                f"{int(vals[-1])} allocation entries reached the fixed-point column-sum "
+                f"range (x >= cs_xmax = {self.dm.struct.cs_xmax:g}); the iterate diverged")
+        if vals[-2]:
+            raise SubproblemError(f"{int(vals[-2])} row subproblems failed to converge")
+        return [int(v) for v in vals[:-2]]
 
     def _launch_chunk(self, iters):
         """One chunk: per iteration price step, fused prox + column sums, and on

@@ -127,3 +127,19 @@ def test_every_row_class_matches_the_oracle(oracle, seed):
     assert np.max(np.abs(eng.x.cpu().numpy() - x)) <= 1e-10 * max(1.0, np.abs(x).max())
     assert np.max(np.abs(eng.p.cpu().numpy() - p)) <= 1e-11 * max(1.0, np.abs(p).max())
     assert np.max(np.abs(eng.xbar.cpu().numpy() - xb)) <= 1e-10 * max(1.0, np.abs(xb).max())
+
+
+@pytest.mark.parametrize("name,row0,nrows", [("c2", 0, None), ("c3", 0, 300_000),
+                                             ("c3", 700_000, 300_000),
+                                             ("c4", 4_000_000, 400_000), ("c5", 0, None)])
+def test_host_regeneration_is_byte_identical(name, row0, nrows):
+    """oracle/market_gen.c rebuilds the device market byte for byte (the CPU
+    reference arm of bench.py builds its instance with it)."""
+    from oracle import gen as hg
+    from paper_2506_06258_b200.generate import generate_config
+
+    d = generate_config(name, seed=0, row0=row0, nrows=nrows)
+    h = hg.generate_config(name, seed=0, row0=row0, nrows=nrows)
+    for k in ("row_ptr", "col", "u", "w"):
+        a = d[k].cpu().numpy()
+        assert a.dtype == h[k].dtype and np.array_equal(a, h[k]), (name, k)

@@ -72,12 +72,12 @@ def test_fixed_point_column_sums_match_fp64():
     assert not np.any(eng.bucket.view(torch.int64).cpu().numpy())  # zeroed after use
 
 
-def test_fixed_point_range_overflow_is_a_fault():
-    from paper_2506_06258_b200.errors import SubproblemError
+def test_fixed_point_range_overflow_is_its_own_error():
+    from paper_2506_06258_b200.errors import FixedPointRangeError
 
     _, eng = _session("solve_medium.npz")
     eng.dm.struct.cs_xmax = 1e-12  # every nonzero x is now out of range
-    with pytest.raises(SubproblemError):
+    with pytest.raises(FixedPointRangeError, match="cs_xmax"):
         eng.run_chunk(1)
 
 

@@ -1,0 +1,125 @@
+"""Screened row solves (working sets) against the unscreened
+fused kernel: the certificate only skips entries the prox keeps at zero, so
+both paths give the same active sets and the same iterate up to the rounding
+of the row sums (different lane groupings), and the same solve."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from _helpers import instance_from
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+
+
+def _pair(gen_kw, steps=(0.05, 0.05)):
+    from paper_2506_06258_b200.device import DeviceMarket
+    from paper_2506_06258_b200.engine import PdhcgEngine
+    from paper_2506_06258_b200.generate import generate_rows
+
+    d = generate_rows(**gen_kw)
+    engs = []
+    for ws in (True, False):
+        dm = DeviceMarket(d["row_ptr"], d["col"], d["u"], d["w"], d["m"])
+        e = PdhcgEngine(dm, working_set=ws)
+        e.initial_state()
+        e.set_steps(*steps)
+        engs.append(e)
+    assert engs[0].working_set and not engs[1].working_set
+    return engs
+
+
+@pytest.mark.parametrize("gen_kw", [
+    dict(n=40_000, m=4_000, q=0.025, seed=5),                       # ~100 entries per row
+    dict(n=60_000, m=8_000, powerlaw=2.0, mean_degree=40.0, seed=2),  # short, medium, long rows
+])
+def test_screened_iterate_equals_unscreened(gen_kw):
+    import torch
+
+    ws, full = _pair(gen_kw)
+    for chunk in (1, 1, 8, 40, 40, 40):
+        ws.run_chunk(chunk)
+        full.run_chunk(chunk)
+        torch.cuda.synchronize()
+        xa, xb = ws.x.cpu().numpy(), full.x.cpu().numpy()
+        pa, pb = ws.p.cpu().numpy(), full.p.cpu().numpy()
+        assert np.array_equal(xa > 0, xb > 0)                  # identical active sets
+        assert np.max(np.abs(xa - xb)) <= 1e-12 * max(1.0, np.max(np.abs(xb)))
+        assert np.max(np.abs(pa - pb)) <= 1e-12 * np.max(np.abs(pb))
+        assert np.array_equal(ws.xflag[:ws.dm.nnz].cpu().numpy().astype(bool), xa > 0)
+    # after the first iterations nearly every tile row is solved over its
+    # working set (rows listed for a full solve in the last iteration)
+    n_full = int(ws.blk_done[3].item())
+    tile_rows = int((ws.ws_init == -1).sum().item())
+    assert n_full <= 0.05 * tile_rows, (n_full, tile_rows)
+    h = ws.ws_len.cpu().numpy()
+    assert np.all(h[ws.ws_init.cpu().numpy() == -3] == -3)
+
+
+def test_restart_and_load_invalidate_the_working_sets():
+    import torch
+
+    ws, _ = _pair(dict(n=20_000, m=2_000, q=0.05, seed=7))
+    ws.run_chunk(40)
+    assert int((ws.ws_len >= 0).sum().item()) > 0
+    ws.restart()
+    torch.cuda.synchronize()
+    assert torch.equal(ws.ws_len, ws.ws_init)
+    ws.run_chunk(40)
+    ws.load_state(ws.x.clone(), ws.p.clone())
+    assert torch.equal(ws.ws_len, ws.ws_init)
+
+
+def test_working_set_slots_mirror_the_iterate():
+    """Each slot holds (u, x, column, position) of its entry; the nonzero
+    entries of a row with a working set are all in its slots."""
+    import torch
+
+    from paper_2506_06258_b200 import _native as nat
+
+    ws, _ = _pair(dict(n=20_000, m=2_000, q=0.05, seed=8))
+    ws.run_chunk(40)
+    ws.run_chunk(3)
+    torch.cuda.synchronize()
+    K = nat.WS_SLOTS
+    h = ws.ws_len.cpu().numpy()
+    rp = ws.dm.row_ptr.cpu().numpy()
+    u, x, col = ws.dm.u.cpu().numpy(), ws.x.cpu().numpy(), ws.dm.col.cpu().numpy()
+    ux = ws.ws_ux.cpu().numpy().reshape(-1, K, 2)
+    cp = ws.ws_cp.cpu().numpy().reshape(-1, K, 2)
+    rows = np.nonzero(h >= 0)[0]
+    assert len(rows) > 0.9 * len(h)
+    for i in rows[:: max(1, len(rows) // 500)]:
+        k = h[i]
+        pos = cp[i, :k, 1]
+        assert np.all(np.diff(pos) > 0)
+        g = rp[i] + pos
+        assert np.array_equal(cp[i, :k, 0], col[g])
+        assert np.array_equal(ux[i, :k, 0], u[g]) and np.array_equal(ux[i, :k, 1], x[g])
+        nz = np.nonzero(x[rp[i]:rp[i + 1]] > 0)[0]
+        assert set(nz.tolist()) <= set(pos.tolist())
+
+
+@pytest.mark.parametrize("name", ["solve_spec1000.npz", "solve_g200_tol0.npz",
+                                  "solve_medium.npz"])
+def test_solves_identical_with_and_without_working_sets(name):
+    import paper_2506_06258_b200 as mq
+
+    g = golden(name)
+    inst = instance_from(g) if "indptr" in g.files else None
+    if inst is None:
+        inst = mq.generate_fisher(mq.GeneratorConfig(n=1000, m=400, sparsity_u=0.2, seed=0))
+    cfg = dict(tol=float(g["tol"]), subproblem_tol=float(g["subtol"]))
+    a = mq.run_solve(inst, mq.SolveConfig(**cfg, working_set=True), "pdhcg")
+    b = mq.run_solve(inst, mq.SolveConfig(**cfg, working_set=False), "pdhcg")
+    assert a.inner_iterations == b.inner_iterations == int(g["iters"])
+    assert a.restarts == b.restarts == int(g["restarts"])
+    assert np.max(np.abs(a.prices - b.prices) / np.abs(b.prices)) <= 1e-9

@@ -158,3 +158,50 @@ def test_generator_fingerprints_match_reference():
         assert mq.instance_fingerprint(inst) == rec["fingerprint"], key
         checked += 1
     assert checked >= 6
+
+
+def test_generator_math_matches_libm():
+    """The bit-specified log / exp of the generator (restated from
+    csrc/mq_genmath.cuh) agree with libm to an ulp or two."""
+    import math
+
+    from oracle import gen as hg
+
+    rng = np.random.default_rng(0)
+    xs = np.concatenate([rng.random(2000), 10.0 ** rng.uniform(-300, 300, 2000)])
+    for x in xs:
+        assert abs(hg.gm_log(x) - math.log(x)) <= 4e-16 * max(1.0, abs(math.log(x)))
+    for y in rng.uniform(-700, 700, 2000):
+        assert abs(hg.gm_exp(y) / math.exp(y) - 1.0) <= 4e-16
+
+
+def test_host_generator_independent_of_threads_and_slicing():
+    from oracle import gen as hg
+
+    a = hg.generate_rows(20_000, 3_000, seed=3, q=0.01, threads=1)
+    b = hg.generate_rows(20_000, 3_000, seed=3, q=0.01, threads=7)
+    for k in ("row_ptr", "col", "u", "w"):
+        assert np.array_equal(a[k], b[k])
+    part = hg.generate_rows(20_000, 3_000, seed=3, q=0.01, row0=7_000, nrows=5_000)
+    rp = a["row_ptr"]
+    lo, hi = rp[7_000], rp[12_000]
+    assert np.array_equal(part["row_ptr"], rp[7_000:12_001] - lo)
+    assert np.array_equal(part["col"], a["col"][lo:hi])
+    assert np.array_equal(part["u"], a["u"][lo:hi])
+    # valid support: ascending columns, values in (0, 1], ~1% density
+    deg = np.diff(rp)
+    assert deg.min() >= 1 and abs(deg.mean() - 30.0) < 1.0
+    starts = rp[:-1]
+    d = np.diff(a["col"].astype(np.int64))
+    inner = np.ones(len(d), dtype=bool)
+    inner[starts[1:] - 1] = False
+    assert (d[inner] > 0).all()
+    assert 0.0 < a["u"].min() and a["u"].max() <= 1.0
+
+
+def test_host_powerlaw_generator_is_heavy_tailed():
+    from oracle import gen as hg
+
+    d = hg.generate_rows(200_000, 50_000, seed=0, powerlaw=2.0, mean_degree=100.0)
+    deg = np.diff(d["row_ptr"])
+    assert 85 < deg.mean() < 115 and deg.max() > 10_000 and np.median(deg) < 40
