@@ -177,39 +177,61 @@ def run_iters(eng, iters, chunk=40):
 
 
 def kernel_breakdown(eng, iters):
-    """Per-kernel device time inside real iterations (eager launches, CUDA
-    events on the launching stream)."""
+    """Per-kernel device time inside real iterations, launched exactly as the
+    engine's chunk does it (eager; CUDA events on the launching stream), and
+    the working-set counts of those iterations."""
     import torch
 
-    from paper_2506_06258_b200 import _native as nat
-
-    lib, mk, st = eng.ops.lib, eng.dm.struct, eng.state
+    ops = eng.ops
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(iters)]
+    full_rows = torch.zeros(1, dtype=torch.int64, device=eng.dm.device)
     eng.pass_buf.zero_()
     eng.faults.zero_()
     for it in range(iters):
-        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         e = ev[it]
         e[0].record()
-        nat.check(lib.mq_dual_step(mk, st, it, s), "dual")
+        ops.dual(it)
         e[1].record()
-        nat.check(lib.mq_primal_step(mk, st, it, None, s), "primal")
+        ops.primal(it)
         e[2].record()
-        nat.check(lib.mq_colsum_step(mk, st, it, 1, s), "colsum")
-        if eng.world > 1:
-            eng._allreduce(eng.cs)
-            nat.check(lib.mq_colsum_finalize(mk, st, it, s), "finalize")
+        if eng.world > 1:  # the engine's N-rank step: integer all-reduce, then convert
+            eng._allreduce(eng.bucket.view(torch.int64)[:eng.dm.m])
+        ops.colsum_rest(it, True)
         e[3].record()
-    cur = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    nat.check(lib.mq_chunk_end(st, iters, cur), "chunk_end")
-    if eng.sparse:
-        nat.check(lib.mq_avg_materialize(mk, st, cur), "avg_materialize")
+        if eng.working_set:
+            full_rows += eng.blk_done[3]
+    ops.chunk_end(iters)
     torch.cuda.synchronize()
     eng.navg += iters
     t = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])]
                   for e in ev])
-    passes = int(eng.pass_buf[:iters].sum().item())
-    return t.mean(axis=0), passes
+    counts = {"passes": int(eng.pass_buf[:iters].sum().item())}
+    if eng.working_set:
+        h = eng.ws_len
+        counts.update(full_rows=float(full_rows.item()) / iters,
+                      ws_entries=int(h.clamp(min=0).sum().item()),
+                      ws_rows=int((h >= 0).sum().item()),
+                      tile_rows=int((eng.ws_init == -1).sum().item()),
+                      nonzero=int(eng.xflag[:eng.dm.nnz].sum().item()))
+    return t.mean(axis=0), counts
+
+
+def screened_bytes(dm, c):
+    """Algorithmic bytes of one screened iteration: what the
+    working-set algorithm must touch once — per tile row its working-set
+    length (4 B) and, with a working set, budget, warm start r/w, certificate
+    and row offset (56 B); per working-set entry its slot (24 B) and price
+    (8 B); per nonzero entry its x write, running-sum r/w and column-sum add
+    (32 B); rows solved in full and the medium / long rows read u, col, flag
+    and price (21 B per entry, 64 B per row); per good 48 B."""
+    rp = dm.row_ptr
+    lens = (rp[1:] - rp[:-1])
+    big = lens > 128
+    big_entries = int(lens[big].sum().item())
+    big_rows = int(big.sum().item())
+    full_entries = c["full_rows"] * (dm.nnz - big_entries) / max(1, c["tile_rows"])
+    return (4 * c["tile_rows"] + 56 * c["ws_rows"] + 32 * c["ws_entries"] + 32 * c["nonzero"]
+            + 21 * (big_entries + full_entries) + 64 * (big_rows + c["full_rows"]) + 48 * dm.m)
 
 
 # random 8-byte gathers from an L2-resident 800 KB vector, 148 SMs, 164 KB of
@@ -237,7 +259,7 @@ def host_copy(shard):
 
     return {"row_ptr": shard["row_ptr"].cpu().numpy(), "col": to_host(shard["col"]),
             "u": to_host(shard["u"]), "w": shard["w"].cpu().numpy(), "n": shard["n"],
-            "m": shard["m"]}
+            "m": shard["m"], "row0": shard["row0"]}
 
 
 def cpu_chunk_run(host, threads):
@@ -286,7 +308,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-max-iters", type=int, default=2000)
+    ap.add_argument("--e2e-max-iters", type=int, default=100_000)
     ap.add_argument("--breakdown-iters", type=int, default=20)
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
@@ -343,30 +365,33 @@ def main():
     if world > 1:
         dist.barrier()
     value = a.steps / (t_ms / 1e3)
-    # kernels launched in the timed region: dual + non-empty primal bins + colsum
-    # per iteration, chunk_end (+ the running-average materialization) per chunk
-    # (+ finalize on N>1)
-    primal_kernels = (int(dm.tiles.shape[0] > 0) + int(dm.long_rows.numel() > 0)
-                      + int(dm.med_rows.numel() > 0))
-    per_it = 2 + primal_kernels + (1 if world > 1 else 0)
-    launches = a.steps * per_it + -(-a.steps // 40) * (1 + int(eng.sparse))
+    # our kernels launched in the timed region, per iteration: dual, the
+    # screened solve + full-solve list (or the tile kernel), medium / long
+    # row kernels where present, column sums; per chunk: chunk_end and the
+    # running-average materialization
+    primal_kernels = ((2 if eng.working_set else int(dm.tiles.shape[0] > 0))
+                      + int(dm.long_rows.numel() > 0) + int(dm.med_rows.numel() > 0))
+    launches = a.steps * (2 + primal_kernels) + -(-a.steps // 40) * (1 + int(eng.sparse))
 
-    # per-kernel breakdown and the primal kernel's roofline
-    kt, kpass = kernel_breakdown(eng, a.breakdown_iters)
-    n_local = dm.n
-    # algorithmic bytes of one iteration's nnz sweep in the dense formulation
-    # (prox + averages 44 B/nnz, column sums 12 B/nnz, + rows and
-    # goods).  The default kernel skips the ~99 % zero entries of x (sparse
-    # iterate), so its DRAM traffic is far lower (`dram_*`);
-    # its binding resource is the random L2 gather of p[col], one 32-byte
-    # sector per entry (`gather_*`, peak = tools/micro/gather_l1.cu)
-    primal_bytes = 56 * nnz_local + 20 * n_local + 8 * m
-    achieved = primal_bytes / (kt[1] / 1e3) / 1e9
+    # per-kernel breakdown (CUDA events, the engine's own launch sequence)
+    kt, counts = kernel_breakdown(eng, a.breakdown_iters)
+    t_primal = kt[1] / 1e3
+    iter_bytes = 56 * nnz_full + 16 * n_full + 48 * m      # SURVEY §8(d) B_iter (dense)
+    if eng.working_set:
+        alg = screened_bytes(dm, counts)
+        rkernel = ("primal step: ws_kernel (screened exact prox over the working sets, "
+                   "averages, column sums) + ws_full_kernel (listed rows) + medium / long row "
+                   "kernels where present")
+        model = ("algorithmic bytes of the screened iteration (DESIGN.md §7): 4 B per tile "
+                 "row, 56 B per row with a working set, 32 B per working-set entry, 32 B per "
+                 "nonzero entry, 21 B per entry of rows solved in full (+64 B per row), 48 B "
+                 "per good; counts measured on the breakdown iterations")
+    else:
+        alg = 56 * dm.nnz + 20 * dm.n + 8 * m
+        rkernel = "primal step: primal_fused_kernel + medium / long row kernels"
+        model = "SURVEY 8(d) dense-formulation bytes"
+    achieved = alg / t_primal / 1e9
     traffic = traffic_from_profile("primal", a.config)
-    gathers_per_s = nnz_local / (kt[1] / 1e3)
-    iter_bytes = 56 * nnz_full + 16 * n_full + 48 * m      # SURVEY §8(d) B_iter
-    iter_gbs = iter_bytes / (t_ms / 1e3 / a.steps) / 1e9 / world
-
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "iter/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t_ms / a.steps, 4),
@@ -374,33 +399,26 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"BASELINE config {a.config[1]}: {CONFIG_TEXT[a.config]}",
                    "n_buyers": n_full, "m_goods": m, "nnz": nnz_full, "seed": a.seed,
-                   "row_solver": "exact", "parallelism": f"row-shard x{world}",
-                   "l2": f"inputs larger than L2 ({iter_bytes / 1e9:.1f} GB algorithmic "
-                         "traffic per iteration vs 126 MB L2)"},
-        "roofline": {"bound": "hbm",
-                     "kernel": "primal step: primal_fused_kernel (exact prox + averages + "
-                               "column sums) + medium / long row kernels where present",
+                   "row_solver": "exact", "working_set": bool(eng.working_set),
+                   "parallelism": f"row-shard x{world}",
+                   "l2": "inputs larger than L2 (8 GB of utilities per GPU vs 126 MB L2)"},
+        "roofline": {"bound": "hbm", "kernel": rkernel,
                      "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": round(achieved / hbm_peak, 4),
-                     "traffic": traffic, "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": primal_bytes,
-                     "note": "achieved = SURVEY 8(d) algorithmic bytes (dense formulation) / "
-                             "kernel time; the sparse-iterate kernel does not move the zero "
-                             "entries of x, see dram_* for its own traffic and gather_* for "
-                             "the resource that binds it",
-                     "dram_achieved": (round(traffic / (kt[1] / 1e3) / 1e9, 1)
-                                       if traffic else None),
-                     "dram_frac": (round(traffic / (kt[1] / 1e3) / 1e9 / hbm_peak, 4)
-                                   if traffic else None),
-                     "gather_achieved": round(gathers_per_s / 1e9, 1),
-                     "gather_peak": GATHER_PEAK / 1e9, "gather_unit": "G random 8-byte L2 "
-                     "gathers/s", "gather_frac": round(gathers_per_s / GATHER_PEAK, 4)},
-        "iteration_roofline": {"bytes_per_iteration": iter_bytes,
-                               "achieved_gbs_per_gpu": round(iter_gbs, 1),
-                               "frac": round(iter_gbs / hbm_peak, 4)},
+                     "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                     "peak_kind": peak_kind, "algorithmic_bytes_per_launch": int(alg),
+                     "model": model,
+                     "dram_achieved": (round(traffic / t_primal / 1e9, 1) if traffic else None),
+                     "dram_frac": (round(traffic / t_primal / 1e9 / hbm_peak, 4)
+                                   if traffic else None)},
+        "dense_equivalent": {"bytes_per_iteration": iter_bytes,
+                             "gbs_per_gpu": round(iter_bytes / (t_ms / 1e3 / a.steps) / 1e9
+                                                  / world, 1),
+                             "note": "SURVEY 8(d) dense-formulation bytes / iteration time: "
+                                     "an equivalent throughput, not bandwidth (the screened "
+                                     "iteration does not move the entries it certifies)"},
         "kernels_ms": {"dual": round(kt[0], 4), "primal": round(kt[1], 4),
                        "colsum": round(kt[2], 4)},
-        "sweeps_per_row_per_iter": round(passes / a.steps / n_full, 3),
+        "working_set": counts, "sweeps_per_row_per_iter": round(passes / a.steps / n_full, 3),
         "gpu_launches": launches, "setup_seconds": round(setup_s, 2),
     }
     with torch.cuda.device(local):
@@ -408,12 +426,17 @@ def main():
     del eng, dm
     torch.cuda.empty_cache()
 
+    host = None
+    if not (a.no_e2e and a.no_cpu):
+        host = host_copy(shard)
+    del shard
+    torch.cuda.empty_cache()
     out["e2e"] = None
-    if world == 1 and not a.no_e2e:
-        out["e2e"] = e2e_solve(shard, a.e2e_max_iters)
+    if not a.no_e2e:
+        out["e2e"] = e2e_solve(host, a.e2e_max_iters, group=group if world > 1 else None)
         out["ttt_seconds"] = out["e2e"]["ttt_seconds"]
     if rank == 0 and world == 1 and not a.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(shard, m, nnz_full)
+        out["cpu_baseline"] = cpu_baseline(host)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -432,8 +455,12 @@ def e2e_solve(host, max_iters, group=None):
     import paper_2506_06258_b200 as mq
 
     n, m = host["n"], host["m"]
-    inst = mq.FisherInstance(mq.SparseMatrix(host["row_ptr"].shape[0] - 1, m, host["row_ptr"],
-                                             host["col"], host["u"]), host["w"])
+    sm = mq.SparseMatrix(host["row_ptr"].shape[0] - 1, m, host["row_ptr"], host["col"],
+                         host["u"])
+    if group is None:
+        inst = mq.FisherInstance(sm, host["w"])
+    else:  # this rank's rows: the public multi-GPU input
+        inst = mq.FisherShard(sm, host["w"], host["row0"], n)
     cfg = mq.SolveConfig(tol=1e-4, max_iters=max_iters, group=group)
     torch.cuda.synchronize()
     t0 = time.perf_counter()

@@ -38,7 +38,7 @@ extern "C" {
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
 #define MQ_REG_ROW 128        /* tile rows longer than this (medium rows) are
                                  solved by the warp-per-row path          */
-#define MQ_WS_SLOTS 16        /* working-set slots per row (screened solve)  */
+#define MQ_WS_SLOTS 12        /* working-set slots per row (screened solve)  */
 
 /* Read-only market description (device pointers, borrowed).  Arrays marked
  * [pad] must have 16 readable bytes past their last element (TMA bulk copies
@@ -95,7 +95,8 @@ typedef struct mq_state {
     double *csbar;    /* [m]   colsum(xbar)                                    */
     int32_t *blk_done;/* [8] the primal kernels' dynamic work counters (tiles,
                          long rows, medium rows, full-solve list length, its
-                         claim counter), zeroed by mq_primal_step            */
+                         claim counter, screened-solve batches), zeroed by
+                         mq_primal_step                                      */
     const double *steps; /* [2] tau, sigma (device-resident: one graph serves
                             every step size)                                   */
     int64_t *navg;    /* [1]  inner iterations since the last restart          */
@@ -113,28 +114,43 @@ typedef struct mq_state {
        whenever it writes x, xbar or navg itself.                            */
     uint8_t *xflag;   /* [nnz] [pad]                                          */
     double *xsum;     /* [nnz]                                                */
-    /* Working set of the screened row solve; ws_len == NULL
+    /* Working set of the screened row solve; ws_hdr == NULL
        selects the unscreened tile kernel.  For a zero entry x_ij = 0, the
        prox keeps it at zero iff p_j s_i >= w_i u_ij (s_i = the row's root),
        so a row is solved over its working set only — nonzero and "near"
        entries, at most MQ_WS_SLOTS, held in slots — and the result is the
        full row's when the certificate
-           theta_i (1 - D / P_i) s >= w_i (1 + 1e-12)
+           theta_i s (P_i - D) >= w_i P_i (1 + 1e-12)
        holds, theta_i = min p_j / u_ij and P_i = min p_j over the screened
        entries at the working set's last rebuild and D the accumulated price
-       decrease since (drift); otherwise (and when ws_len < 0) the row is
-       solved in full and its working set rebuilt.  ws_len[i]: slots in use
-       (>= 0); -1 no valid working set; -2 larger than MQ_WS_SLOTS (solved in
-       full every iteration); -3 not a tile row (medium / long kernels).  The
-       host writes -1 (keeping -3) whenever it writes x or p itself.       */
-    int32_t *ws_len;  /* [n]                                                  */
-    double *ws_cert;  /* [4n] theta, P, C at the rebuild, unused             */
-    double *ws_ux;    /* [2 n MQ_WS_SLOTS] (u, x) per slot, ascending entry  */
-    int32_t *ws_cp;   /* [2 n MQ_WS_SLOTS] (column, entry offset in the row) */
+       decrease since (drift); otherwise (and when h < 0) the row is solved in
+       full and its working set rebuilt.  Rows are grouped in blocks of 32
+       (block b = rows 32b..32b+31), the unit of the screened kernel's
+       bulk copies.  The host writes h = -1 (keeping -3) and kmax = 0
+       whenever it writes x or p itself.                                   */
+    int32_t *ws_hdr;  /* [4 npad] per row: h = slots in use (>= 0), -1 none,
+                         -2 more than MQ_WS_SLOTS (solved in full every
+                         iteration), -3 not a tile row (medium / long
+                         kernels); then theta, P, C at the rebuild as float
+                         bit patterns, each rounded down                     */
+    int32_t *ws_kmax; /* [npad / 32] upper bound of h over each block of 32
+                         rows (the screened kernel copies slots 0..kmax-1) */
+    /* slots, ascending entry order within a row; slot k of row i at
+       ((i / 32) * MQ_WS_SLOTS + k) * 32 + i % 32 (a block's slots 0..k are
+       one contiguous run); arrays of npad * MQ_WS_SLOTS, npad = n rounded
+       up to 32                                                             */
+    double *ws_u;     /* normalized utility of the slot's entry              */
+    double *ws_x;     /* its current x (the slot is authoritative)           */
+    int32_t *ws_col;  /* its good                                            */
+    uint8_t *ws_pos;  /* its offset in the row (tile rows <= MQ_REG_ROW)     */
     int32_t *ws_list; /* [n] rows solved in full this iteration               */
     double *drift;    /* [2] C = accumulated bound on the largest price
                          decrease (rounded up), this iteration's decrease
                          (bit pattern, order-free max)                      */
+    int32_t ws_rebuild; /* nonzero: this step runs the unscreened tile kernel
+                           over every tile row and rebuilds all working sets
+                           (after the host invalidated them; cheaper than
+                           the per-row full solves when every row needs one) */
 } mq_state;
 
 /* Mutable iterate of the lifted PDHG path (algo="pdhg", kernels.py:146-197):

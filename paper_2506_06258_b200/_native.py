@@ -19,7 +19,7 @@ REG_ROW = 128         # MQ_REG_ROW
 TILE_ROWS = 256       # MQ_TILE_ROWS
 PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
 ABI_VERSION = 8
-WS_SLOTS = 16          # MQ_WS_SLOTS
+WS_SLOTS = 12          # MQ_WS_SLOTS
 
 _lock = threading.Lock()
 _lib = None
@@ -52,8 +52,9 @@ class MqState(ctypes.Structure):
     _fields_ = [("x", P), ("xbar", P), ("p", P), ("pbar", P), ("cs", P), ("cs_prev", P),
                 ("csbar", P), ("blk_done", P), ("steps", P), ("navg", P),
                 ("pass_out", P), ("faults", P), ("bucket", P), ("srow", P),
-                ("xflag", P), ("xsum", P), ("ws_len", P), ("ws_cert", P), ("ws_ux", P),
-                ("ws_cp", P), ("ws_list", P), ("drift", P)]
+                ("xflag", P), ("xsum", P), ("ws_hdr", P), ("ws_kmax", P), ("ws_u", P),
+                ("ws_x", P), ("ws_col", P), ("ws_pos", P), ("ws_list", P), ("drift", P),
+                ("ws_rebuild", ctypes.c_int32)]
 
 
 PM = ctypes.POINTER(MqMarket)

@@ -399,6 +399,115 @@ __device__ __forceinline__ double row_root_warm(const double (&c)[PER], const do
     return s;
 }
 
+// ------------------------------------------------------------ working sets
+// Safe screening of the row solve (DESIGN.md §5.1, include/market_eq_b200.h
+// mq_state.ws_*).  A zero entry stays zero through the prox iff
+// c s + tau w u <= 0 with c = -tau p, i.e. p s >= w u: inactive entries never
+// enter the root (masked) nor change.  A row whose zero entries satisfy that
+// with margin at the row's root can therefore be solved over the rest —
+// its working set: the nonzero entries plus the zero entries within a factor
+// MQ_WS_GAMMA of the threshold — and gives exactly the full row's active set,
+// root and allocation.  The certificate needs no look at the screened
+// entries: their prices have dropped by at most D (drift) since the working
+// set was built, so p_j s >= (p_j^ref - D) s >= theta (1 - D / P) s with
+// theta = min p^ref / u and P = min p^ref over them.  On C4 the working sets
+// hold ~5 % of the entries and the certificate holds for ~100 % of the rows
+// (tools/screen_stats.py, tools/ws_stats.py): one price gather in ~20 instead
+// of every entry's.
+#ifndef MQ_WS_GAMMA
+#define MQ_WS_GAMMA 1.03
+#endif
+#ifndef MQ_WS_MARGIN
+#define MQ_WS_MARGIN 1e-12
+#endif
+
+// slot k of row i: a warp's 32 consecutive rows read slot k as one run
+__device__ __forceinline__ int64_t ws_at(int64_t i, int k) {
+    return (((i >> 5) * MQ_WS_SLOTS + k) << 5) + (i & 31);
+}
+
+// Append `row` to this iteration's full-solve list (warp-aggregated).  The
+// list order is irrelevant to the results: rows are independent and the
+// column sums are order-free.
+__device__ __forceinline__ void ws_push(const mq_state &st, bool push, int64_t row) {
+    const uint32_t b = __ballot_sync(MQ_FULL, push);
+    if (!b) return;
+    const int wl = threadIdx.x & 31;
+    const int leader = __ffs(b) - 1;
+    int base = 0;
+    if (wl == leader) base = atomicAdd(st.blk_done + 3, __popc(b));
+    base = __shfl_sync(MQ_FULL, base, leader);
+    if (push) st.ws_list[base + __popc(b & ((1u << wl) - 1u))] = (int32_t)row;
+}
+
+// price-decrease bound of this iteration: C + dec, rounded up (the value the
+// column-sum kernel stores as the next C)
+__device__ __forceinline__ double drift_now(const mq_state &st) {
+    return __dadd_ru(st.drift[0], st.drift[1]);
+}
+
+// Rebuild row i's working set after its full solve (G lanes, entry t = lane
+// + G e in register e): the nonzero entries and the zero entries near the
+// threshold (p s < gamma w u) take slots in ascending entry order; theta =
+// min p / u and P = min p over the rest, C = the drift now.  More than
+// MQ_WS_SLOTS working entries: h = -2 (solved in full next time).
+template <int G, int RP>
+__device__ __forceinline__ void ws_build(const mq_state &st, int64_t i, int lane, int gsub,
+                                         bool build, int len, double w, double s, double cnow,
+                                         const double (&u)[RP], const double (&pv)[RP],
+                                         const double (&xn)[RP], const int (&jc)[RP]) {
+    constexpr int K = MQ_WS_SLOTS;
+    const double gw = MQ_WS_GAMMA * w;
+    int before = 0, rank[RP];
+    uint32_t hot = 0;
+    // smallest p / u over the screened entries: the pair is picked by
+    // cross-multiplication and divided once (rounded down, less 2 ulp); a
+    // pick off by an ulp is far inside the certificate's 1e-12 margin
+    double bp = CUDART_INF, bu = 1.0, pm = CUDART_INF;
+#pragma unroll
+    for (int e = 0; e < RP; ++e) {
+        const int t = lane + e * G;
+        const bool in = build && t < len;
+        const bool hb = in && (xn[e] > 0.0 || pv[e] * s < gw * u[e]);
+        if (hb) hot |= 1u << e;
+        if (in && !hb) {
+            if (pv[e] * bu < bp * u[e]) {
+                bp = pv[e];
+                bu = u[e];
+            }
+            pm = fmin(pm, pv[e]);
+        }
+        const uint32_t bal = (__ballot_sync(MQ_FULL, hb) >> (gsub * G)) & ((1u << G) - 1u);
+        rank[e] = before + __popc(bal & ((1u << lane) - 1u));
+        before += __popc(bal);
+    }
+    double th = bp == CUDART_INF ? CUDART_INF : __ddiv_rd(bp, bu) * (1.0 - 4e-16);
+    th = group_min<G>(th);
+    pm = group_min<G>(pm);
+    if (!build) return;
+    if (before <= K) {
+#pragma unroll
+        for (int e = 0; e < RP; ++e) {
+            if ((hot >> e) & 1u) {
+                const int64_t at = ws_at(i, rank[e]);
+                st.ws_u[at] = u[e];
+                st.ws_x[at] = xn[e];
+                st.ws_col[at] = jc[e];
+                st.ws_pos[at] = (uint8_t)(lane + e * G);
+            }
+        }
+        if (lane == 0) {
+            reinterpret_cast<int4 *>(st.ws_hdr)[i] =
+                make_int4(before, __float_as_int(__double2float_rd(th)),
+                          __float_as_int(__double2float_rd(pm)),
+                          __float_as_int(__double2float_rd(cnow)));
+            atomicMax(st.ws_kmax + (i >> 5), before);
+        }
+    } else if (lane == 0) {
+        st.ws_hdr[4 * i] = -2;
+    }
+}
+
 // ------------------------------------------------------------ primal (fused)
 template <int ETILE, int RTILE>
 struct TileLayout {
@@ -420,7 +529,7 @@ struct TileLayout {
 // landed; empty[s]: every solver warp is done with it.  Solver warps claim
 // row pairs from a shared counter, so no solver waits for another inside a
 // tile.
-template <int G, int NSW, int ETILE, int RTILE, int NSTAGE>
+template <int G, int NSW, int ETILE, int RTILE, int NSTAGE, bool BUILD>
 __global__ void __launch_bounds__((NSW + 1) * 32, 1)
 primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
                     int64_t tile_lo, int64_t tile_hi, int *tile_ctr) {
@@ -605,13 +714,18 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 if (has && lane == 0) st.srow[r0 + r] = sr;
                 const double inv_s = 1.0 / sr;
                 MQ_TS(tq2);
+                double xn[RP];
+                int jc[RP];
 #pragma unroll
                 for (int e = 0; e < RP; ++e) {
                     const int t = a + lane + e * G;
-                    if (t < b)
-                        put_x(mk, st, e0 + t, scol[t], fmax(c[e] + tw * u[e] * inv_s, 0.0),
-                              (fb >> e) & 1u);
+                    xn[e] = t < b ? fmax(c[e] + tw * u[e] * inv_s, 0.0) : 0.0;
+                    jc[e] = t < b ? scol[t] : 0;
+                    if (t < b) put_x(mk, st, e0 + t, jc[e], xn[e], (fb >> e) & 1u);
                 }
+                if (BUILD)  // the working sets of every row, rebuilt at once
+                    ws_build<G, RP>(st, r0 + r, lane, gsub, has, b - a, has ? sw[r] : 0.0, sr,
+                                    drift_now(st), u, pv, xn, jc);
                 MQ_TS(tq3);
                 MQ_TA(5, tq0, tq1);
                 MQ_TA(6, tq1, tq2);
@@ -656,7 +770,10 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                 const double B = group_sum<G>(bp);
                 const double sr =
                     row_root_exact<G>(su, sc, a, b, lane, tw, s0, A, B, has, &nsw, &ok);
-                if (has && !med && lane == 0) st.srow[r0 + r] = sr;
+                if (has && !med && lane == 0) {
+                    st.srow[r0 + r] = sr;
+                    if (BUILD) st.ws_hdr[4 * (r0 + r)] = -1;  // full solve next time
+                }
                 const double inv_s = 1.0 / sr;
                 for (int t0 = a + lane; t0 < b; t0 += MQ_LB * G) {
                     double cv[MQ_LB];
@@ -988,145 +1105,282 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
         atomicAdd((unsigned long long *)st.faults, (unsigned long long)my_faults);
 }
 
-// ------------------------------------------------------------ working set
-// Safe screening of the row solve (DESIGN.md §5.1, include/market_eq_b200.h
-// mq_state.ws_*).  A zero entry stays zero through the prox iff
-// c s + tau w u <= 0 with c = -tau p, i.e. p s >= w u: inactive entries never
-// enter the root (masked) nor change.  A row whose zero entries satisfy that
-// with margin at the row's root can therefore be solved over the rest —
-// its working set: the nonzero entries plus the zero entries within a factor
-// MQ_WS_GAMMA of the threshold — and gives exactly the full row's active set,
-// root and allocation.  The certificate needs no look at the screened
-// entries: their prices have dropped by at most D (drift) since the working
-// set was built, so p_j s >= (p_j^ref - D) s >= theta (1 - D / P) s with
-// theta = min p^ref / u and P = min p^ref over them.  On C4 the working sets
-// hold ~6 % of the entries and the certificate holds for ~100 % of the rows
-// (tools/screen_stats.py): one price gather in ~16 instead of every entry's.
-#ifndef MQ_WS_GAMMA
-#define MQ_WS_GAMMA 1.05
+// Screened solve over 32-row blocks, one thread per row, fed by a TMA
+// producer warp.  The producer claims batches of MQ_WS_SB consecutive blocks
+// and bulk-copies each into a shared-memory stage: the rows' headers (h,
+// theta, P, C), budgets, warm starts and row offsets, and each block's slots
+// 0..kmax-1 (u, x, column, position: one contiguous run per array).  MQ_WS_NC consumer warps claim
+// blocks of the current stage and solve one row per thread: the only round
+// trip left in a row's chain is the price gather of its working entries.
+// The root is the monotone active-set iteration of row_root_warm run
+// serially on the thread's row (no shuffles); the certificate
+// theta s (P - D) >= w P (1 + margin) is evaluated in directed rounding
+// (left side down, right side up).  Rows without a working set, or whose
+// certificate fails, go to the full-solve list untouched.
+#ifndef MQ_WS_NC
+#define MQ_WS_NC 15  // consumer warps per CTA (one CTA per SM; 16 warps: <= 128 registers)
 #endif
-#ifndef MQ_WS_MARGIN
-#define MQ_WS_MARGIN 1e-12
+#ifndef MQ_WS_SB
+#define MQ_WS_SB 4  // 32-row blocks per stage
 #endif
-constexpr int kWsG = 8;                     // lanes per row: 4 rows per warp
-constexpr int kWsPer = MQ_WS_SLOTS / kWsG;  // slots per lane
-
-// Append `row` to this iteration's full-solve list (one lane per row pushes;
-// warp-aggregated).  The list order is irrelevant to the results: rows are
-// independent and the column sums are order-free.
-__device__ __forceinline__ void ws_push(const mq_state &st, bool push, int64_t row) {
-    const uint32_t b = __ballot_sync(MQ_FULL, push);
-    if (!b) return;
-    const int wl = threadIdx.x & 31;
-    const int leader = __ffs(b) - 1;
-    int base = 0;
-    if (wl == leader) base = atomicAdd(st.blk_done + 3, __popc(b));
-    base = __shfl_sync(MQ_FULL, base, leader);
-    if (push) st.ws_list[base + __popc(b & ((1u << wl) - 1u))] = (int32_t)row;
-}
-
-// price-decrease bound of this iteration: C + dec, rounded up (the value the
-// column-sum kernel stores as the next C)
-__device__ __forceinline__ double drift_now(const mq_state &st) {
-    return __dadd_ru(st.drift[0], st.drift[1]);
-}
-
-// Screened solve of every tile row with a working set (ws_len >= 0), 8 lanes
-// per row, slots in registers.  Rows without one, or whose certificate
-// fails, go to the full-solve list untouched.
-#ifndef MQ_WS_MINB
-#define MQ_WS_MINB 3  // resident 256-thread CTAs per SM of the screened solve
+#ifndef MQ_WS_NST
+#define MQ_WS_NST 4  // stages
 #endif
-__global__ void __launch_bounds__(256, MQ_WS_MINB)
+template <int K, int SB>
+struct WsStage {
+    int4 hdr[SB * 32];  // h, theta, P, C (float bits)
+    double w[SB * 32];
+    double srow[SB * 32];
+    long long rp[SB * 32];  // row offsets
+    // slots of the stage's SB blocks, block e's slot k of row l at
+    // (e * K + k) * 32 + l (the global layout); block e's slots 0..kmax-1
+    // arrive with one copy per array
+    double u[SB * K * 32];
+    double x[SB * K * 32];
+    int32_t col[SB * K * 32];
+    uint8_t pos[SB * K * 32];
+};
+using WsStageT = WsStage<MQ_WS_SLOTS, MQ_WS_SB>;
+constexpr int kWsSmem = MQ_WS_NST * (int)sizeof(WsStageT) + MQ_WS_NST * (2 * 8 + 8 + 4) + 64;
+static_assert(sizeof(WsStageT) % 16 == 0, "stage must keep 16-byte alignment");
+
+__global__ void __launch_bounds__((MQ_WS_NC + 1) * 32, 1)
 ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
-    constexpr int G = kWsG, PER = kWsPer, K = MQ_WS_SLOTS, RPW = 32 / G;
+    constexpr int K = MQ_WS_SLOTS, SB = MQ_WS_SB, NST = MQ_WS_NST, NC = MQ_WS_NC;
+    extern __shared__ __align__(128) unsigned char wsm[];
+    WsStageT *stg = reinterpret_cast<WsStageT *>(wsm);
+    uint64_t *full = reinterpret_cast<uint64_t *>(wsm + NST * sizeof(WsStageT));
+    uint64_t *empty = full + NST;
+    int64_t *sblk = reinterpret_cast<int64_t *>(empty + NST);  // first block of each stage
+    int *claim = reinterpret_cast<int *>(sblk + NST);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < NST; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], NC);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t nblk = (mk.n + 31) >> 5;
+    const int64_t nbatch = (nblk + SB - 1) / SB;
+
+    if (warp == NC) {  // ------------------------------------------- producer
+        if (lane == 0) {
+            // batches claimed from a global counter one step ahead (dynamic
+            // claims balance the CTAs), with their blocks' kmax
+            const uint64_t pol = policy_evict_first();
+            int *ctr = st.blk_done + 5;
+            auto load_km = [&](int64_t bt, int (&km)[SB]) {
+                for (int e = 0; e < SB; ++e)
+                    km[e] = (bt < nbatch && bt * SB + e < nblk) ? __ldcg(st.ws_kmax + bt * SB + e)
+                                                                 : 0;
+            };
+            int64_t bnx = atomicAdd(ctr, 1);
+            int kmn[SB];
+            load_km(bnx, kmn);
+            for (int64_t j = 0;; ++j) {
+                const int q = (int)(j % NST);
+                const int64_t bt = bnx;
+                int km[SB];
+                for (int e = 0; e < SB; ++e) km[e] = kmn[e];
+                if (bt < nbatch) {
+                    bnx = atomicAdd(ctr, 1);
+                    load_km(bnx, kmn);
+                }
+                if (j >= NST) mbar_wait(&empty[q], (uint32_t)(((j / NST) - 1) & 1));
+                claim[q] = 0;
+                if (bt >= nbatch) {  // sentinel: the consumers leave
+                    sblk[q] = -1;
+                    mbar_arrive(&full[q]);
+                    break;
+                }
+                WsStageT &d = stg[q];
+                const int64_t b0 = bt * SB, r0 = b0 * 32;
+                const int64_t rows = mk.n - r0 < SB * 32 ? mk.n - r0 : SB * 32;
+                const int nb = (int)(nblk - b0 < SB ? nblk - b0 : SB);
+                sblk[q] = b0;
+                const uint32_t b16 = (uint32_t)rows * 16u;
+                const uint32_t b8 = ((uint32_t)rows * 8u + 15u) & ~15u;
+                uint32_t tx = b16 + 3 * b8;
+                for (int e = 0; e < nb; ++e) tx += (uint32_t)km[e] * 32u * (8u + 8u + 4u + 1u);
+                mbar_expect_tx(&full[q], tx);
+                bulk_g2s(d.hdr, st.ws_hdr + 4 * r0, b16, &full[q]);
+                bulk_g2s(d.w, mk.w + r0, b8, &full[q]);
+                bulk_g2s(d.srow, st.srow + r0, b8, &full[q]);
+                bulk_g2s(d.rp, mk.row_ptr + r0, b8, &full[q]);
+                for (int e = 0; e < nb; ++e) {
+                    if (!km[e]) continue;
+                    const int64_t o = (b0 + e) * K * 32;
+                    const int so = e * K * 32;
+                    const uint32_t ns = (uint32_t)km[e] * 32u;
+                    bulk_g2s_hint(d.u + so, st.ws_u + o, ns * 8u, &full[q], pol);
+                    bulk_g2s_hint(d.x + so, st.ws_x + o, ns * 8u, &full[q], pol);
+                    bulk_g2s_hint(d.col + so, st.ws_col + o, ns * 4u, &full[q], pol);
+                    bulk_g2s_hint(d.pos + so, st.ws_pos + o, ns, &full[q], pol);
+                }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------ consumers
+    // A consumer copies its block's rows into registers and releases the
+    // stage at once (at most one block per stage and warp: the stage is back
+    // with the producer after a shared-memory read, not after the solve);
+    // the price gathers and the solve then run from registers.
     const double tau = st.steps[0];
     const double cnow = drift_now(st);
-    const int wl = threadIdx.x & 31, lane = wl & (G - 1), gsub = wl / G;
-    const uint32_t gmask = ((1u << G) - 1u) << (gsub * G);
-    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const double2 *__restrict__ ux2 = reinterpret_cast<const double2 *>(st.ws_ux);
-    const int2 *__restrict__ cp2 = reinterpret_cast<const int2 *>(st.ws_cp);
     int my_sweeps = 0;
-    for (int64_t q = warp0; q * RPW < mk.n; q += nwarps) {
-        const int64_t i = q * RPW + gsub;
-        const bool has = i < mk.n;
-        int h = has ? __ldcg(st.ws_len + i) : -3;
+    for (int64_t j = 0;; ++j) {
+        const int q = (int)(j % NST);
+        mbar_wait(&full[q], (uint32_t)((j / NST) & 1));
+        const int64_t b0 = sblk[q];
+        if (b0 < 0) break;
+        const WsStageT &d = stg[q];
+        int e = 0;
+        if (lane == 0) e = atomicAdd(&claim[q], 1);
+        e = __shfl_sync(MQ_FULL, e, 0);
+        const bool mine = e < SB && b0 + e < nblk;  // warp-uniform
+        const int rl = mine ? e * 32 + lane : 0;
+        const int so = mine ? e * K * 32 + lane : 0;
+        const int64_t i = (b0 + (mine ? e : 0)) * 32 + lane;
+        const bool has = mine && i < mk.n;
+        int4 hd = make_int4(-3, 0, 0, 0);
+        double w = 0.0, s0 = 0.0, u[K], c[K], pv[K];
+        int64_t e0 = 0;
+        if (mine) {
+            hd = d.hdr[rl];
+            w = d.w[rl];
+            s0 = d.srow[rl];
+            e0 = d.rp[rl];
+        }
+        int h = has ? hd.x : -3;
         if (force_full && h != -3) h = -1;
-        ws_push(st, has && lane == 0 && (h == -1 || h == -2), i);
-        const bool act = has && h >= 0;
-        double u[PER], c[PER], xo[PER], pv[PER];
-        int jc[PER], pos[PER];
+        uint32_t was = 0;  // slots whose x was nonzero
 #pragma unroll
-        for (int e = 0; e < PER; ++e) {
-            const int slot = lane + e * G;
-            double2 a = make_double2(0.0, 0.0);
-            int2 b = make_int2(0, 0);
-            if (act && slot < h) {
-                a = __ldcg(ux2 + i * K + slot);
-                b = __ldcg(cp2 + i * K + slot);
+        for (int k = 0; k < K; ++k) {  // the price gathers leave before the release
+            u[k] = 0.0;
+            c[k] = 0.0;  // holds x until the gathers return
+            pv[k] = 0.0;
+            if (k < h) {
+                u[k] = d.u[so + k * 32];
+                c[k] = d.x[so + k * 32];
+                pv[k] = __ldg(st.p + d.col[so + k * 32]);
+                if (c[k] > 0.0) was |= 1u << k;
             }
-            u[e] = a.x;
-            xo[e] = a.y;
-            jc[e] = b.x;
-            pos[e] = b.y;
         }
-        double w = 0.0, s0 = 0.0;
-        double2 cert01 = make_double2(0.0, 0.0);
-        double cref = 0.0;
-        if (act) {
-            w = __ldg(mk.w + i);
-            s0 = st.srow[i];
-            cert01 = __ldcg(reinterpret_cast<const double2 *>(st.ws_cert) + 2 * i);
-            cref = __ldcg(st.ws_cert + 4 * i + 2);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[q]);
+        if (!mine) continue;
+        ws_push(st, h == -1 || h == -2, i);
+        const bool act = h >= 0;
 #pragma unroll
-        for (int e = 0; e < PER; ++e) pv[e] = (act && lane + e * G < h) ? __ldg(st.p + jc[e]) : 0.0;
+        for (int k = 0; k < K; ++k) c[k] -= tau * pv[k];
         const double tw = tau * w;
+        // ---- exact root over the working set (row_root_warm, one thread)
+        auto amask = [&](double z) -> uint32_t {
+            uint32_t msk = 0;
 #pragma unroll
-        for (int e = 0; e < PER; ++e) c[e] = xo[e] - tau * pv[e];
+            for (int k = 0; k < K; ++k)
+                if (u[k] > 0.0 && fma(c[k], z, tw * u[k]) > 0.0) msk |= 1u << k;
+            return msk;
+        };
+        auto sums = [&](uint32_t msk, double &A, double &B) {
+            A = 0.0;
+            B = 0.0;
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+                if ((msk >> k) & 1u) {
+                    A += u[k] * c[k];
+                    B += u[k] * u[k];
+                }
+        };
+        double sr = 1.0;
         int nsw = 0;
-        bool ok = true;
-        const double s = row_root_warm<G, PER>(c, u, tw, s0, act, gmask, &nsw, &ok);
-        bool pass = false;
-        if (act && ok) {
-            // directed rounding: lhs rounded down, rhs up (a sound test)
-            const double D = fmax(__dsub_ru(cnow, cref), 0.0);
-            const double f = __dadd_rd(1.0, -__ddiv_ru(D, cert01.y));
-            const double lhs = __dmul_rd(__dmul_rd(cert01.x, f), s);
-            pass = f > 0.0 && lhs >= __dmul_ru(w, 1.0 + MQ_WS_MARGIN);
+        bool ok = act;
+        if (act) {
+            const bool warm = s0 > 0.0;
+            uint32_t prev = amask(warm ? s0 : 0.0);
+            double A, B;
+            sums(prev, A, B);
+            ++nsw;
+            bool force = false, done = false;
+            if (!warm) {
+                if (prev) sr = active_root(A, B, tw);
+                done = prev == 0u;
+                ok = prev != 0u;
+            } else if (fma(A, s0, tw * B) >= s0 * s0) {  // g(s0) >= s0
+                sr = fmax(active_root(A, B, tw), s0);
+            } else {
+                sr = A + tw * B / s0;  // g(s0): a lower bound, active set unknown
+                force = true;
+            }
+            for (int sw = 0; sw < kMaxSweeps && !done; ++sw) {
+                const uint32_t msk = amask(sr);
+                ++nsw;
+                if ((msk == prev && !force) || msk == 0u) {
+                    done = true;
+                    if (msk == 0u) ok = false;
+                } else {
+                    sums(msk, A, B);
+                    sr = fmax(active_root(A, B, tw), sr);
+                    prev = msk;
+                    force = false;
+                }
+            }
+            ok = ok && done;
         }
-        ws_push(st, act && lane == 0 && !pass, i);
-        if (pass) {  // uniform over the row's lanes
-            const int64_t e0 = __ldg(mk.row_ptr + i);
-            const double inv_s = 1.0 / s;
+        bool pass = false;
+        if (ok) {
+            const double th = (double)__int_as_float(hd.y), pm = (double)__int_as_float(hd.z);
+            const double D = fmax(__dsub_ru(cnow, (double)__int_as_float(hd.w)), 0.0);
+            const double lhs = __dmul_rd(__dmul_rd(th, sr), __dsub_rd(pm, D));
+            const double rhs = __dmul_ru(__dmul_ru(w, pm), 1.0 + MQ_WS_MARGIN);
+            pass = lhs >= rhs && pm > D;
+        }
+        ws_push(st, act && !pass, i);
+        if (pass) {
+            const double inv_s = 1.0 / sr;
+            // entries that are or were nonzero: their positions and goods are
+            // fetched together (one round trip), then written
+            uint32_t wm = was;
 #pragma unroll
-            for (int e = 0; e < PER; ++e) {
-                const int slot = lane + e * G;
-                if (slot < h) {
-                    const double xn = fmax(c[e] + tw * u[e] * inv_s, 0.0);
-                    const int64_t g = e0 + pos[e];
-                    if (xn != xo[e]) {
-                        st.ws_ux[2 * (i * K + slot) + 1] = xn;
-                        st.x[g] = xn;
-                        if ((xn > 0.0) != (xo[e] > 0.0)) st_flag(st.xflag + g, xn > 0.0);
-                    }
-                    if (xn > 0.0) {
+            for (int k = 0; k < K; ++k)
+                if (k < h && c[k] + tw * u[k] * inv_s > 0.0) wm |= 1u << k;
+            int pos[K], jc[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                pos[k] = 0;
+                jc[k] = 0;
+                if ((wm >> k) & 1u) {
+                    const int64_t at = ws_at(i, k);
+                    pos[k] = __ldcg(st.ws_pos + at);
+                    jc[k] = __ldcg(st.ws_col + at);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if ((wm >> k) & 1u) {
+                    const double xn = fmax(c[k] + tw * u[k] * inv_s, 0.0);
+                    const bool nz = xn > 0.0, wz = (was >> k) & 1u;
+                    const int64_t g = e0 + pos[k];
+                    st.ws_x[ws_at(i, k)] = xn;
+                    st.x[g] = xn;
+                    if (nz != wz) st_flag(st.xflag + g, nz);
+                    if (nz) {
                         red_add_f64(st.xsum + g, xn);
-                        fixed_colsum_add(mk, st, jc[e], xn);
+                        fixed_colsum_add(mk, st, jc[k], xn);
                     }
                 }
             }
-            if (lane == 0) {
-                st.srow[i] = s;
-                my_sweeps += nsw;
-            }
+            st.srow[i] = sr;
+            my_sweeps += nsw;
         }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) my_sweeps += __shfl_xor_sync(MQ_FULL, my_sweeps, o);
-    if (wl == 0 && my_sweeps)
+    if (lane == 0 && my_sweeps)
         atomicAdd((unsigned long long *)(st.pass_out + it), (unsigned long long)my_sweeps);
 }
 
@@ -1134,16 +1388,17 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
 // than MQ_WS_SLOTS working entries, or x_prev_out requested), 16 lanes per row,
 // the row (<= MQ_REG_ROW entries) in registers, then the working set rebuilt:
 // slots in ascending entry order, theta / P over the screened entries, C.
-__global__ void __launch_bounds__(256)
+#ifndef MQ_WSF_MINB
+#define MQ_WSF_MINB 2  // resident 256-thread CTAs per SM of the full solve
+#endif
+__global__ void __launch_bounds__(256, MQ_WSF_MINB)
 ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
-    constexpr int G = 16, RP = MQ_REG_PER, K = MQ_WS_SLOTS;
+    constexpr int G = 16, RP = MQ_REG_PER;
     const double tau = st.steps[0];
     const double cnow = drift_now(st);
     const int wl = threadIdx.x & 31, lane = wl & (G - 1), gsub = wl / G;
     const uint32_t gmask = ((1u << G) - 1u) << (gsub * G);
     const int count = *(volatile int32_t *)(st.blk_done + 3);
-    double2 *__restrict__ ux2 = reinterpret_cast<double2 *>(st.ws_ux);
-    int2 *__restrict__ cp2 = reinterpret_cast<int2 *>(st.ws_cp);
     int my_sweeps = 0, my_faults = 0;
     for (;;) {
         int rb = 0;
@@ -1162,7 +1417,7 @@ ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict
             len = (int)(__ldg(mk.row_ptr + i + 1) - a);
             w = __ldg(mk.w + i);
             s0 = st.srow[i];
-            hold = __ldcg(st.ws_len + i);
+            hold = __ldcg(st.ws_hdr + 4 * i);
         }
         double c[RP], u[RP], pv[RP], xv[RP];
         int jc[RP];
@@ -1208,47 +1463,7 @@ ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict
                 }
             }
         }
-        // working set: nonzero entries and zero entries near the threshold
-        // (p s < gamma w u), ranked by entry position t = lane + 16 e
-        const bool build = has && hold != -3;
-        const double gw = MQ_WS_GAMMA * w;
-        int before = 0, rank[RP];
-        uint32_t hot = 0;
-        double th = CUDART_INF, pm = CUDART_INF;
-#pragma unroll
-        for (int e = 0; e < RP; ++e) {
-            const int t = lane + e * G;
-            const bool in = build && t < len;
-            const bool hb = in && (xn[e] > 0.0 || pv[e] * s < gw * u[e]);
-            if (hb) hot |= 1u << e;
-            if (in && !hb) {
-                th = fmin(th, __ddiv_rd(pv[e], u[e]));
-                pm = fmin(pm, pv[e]);
-            }
-            const uint32_t bal = (__ballot_sync(MQ_FULL, hb) >> (gsub * G)) & ((1u << G) - 1u);
-            rank[e] = before + __popc(bal & ((1u << lane) - 1u));
-            before += __popc(bal);
-        }
-        th = group_min<G>(th);
-        pm = group_min<G>(pm);
-        if (build) {
-            if (before <= K) {
-#pragma unroll
-                for (int e = 0; e < RP; ++e) {
-                    if ((hot >> e) & 1u) {
-                        ux2[i * K + rank[e]] = make_double2(u[e], xn[e]);
-                        cp2[i * K + rank[e]] = make_int2(jc[e], lane + e * G);
-                    }
-                }
-                if (lane == 0) {
-                    reinterpret_cast<double2 *>(st.ws_cert)[2 * i] = make_double2(th, pm);
-                    st.ws_cert[4 * i + 2] = cnow;
-                    st.ws_len[i] = before;
-                }
-            } else if (lane == 0) {
-                st.ws_len[i] = -2;
-            }
-        }
+        ws_build<G, RP>(st, i, lane, gsub, has && hold != -3, len, w, s, cnow, u, pv, xn, jc);
         if (has && lane == 0) {
             st.srow[i] = s;
             my_sweeps += nsw;
@@ -1335,49 +1550,74 @@ __global__ void avg_materialize_kernel(int64_t nnz, const double *__restrict__ x
 }
 
 // ------------------------------------------------------------ launchers
+// per-device caches: a process may solve on several GPUs (SolveConfig.device)
 static int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+    static int n[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int k = dev & 63;
+    if (!n[k]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        n[k] = v > 0 ? v : 148;
     }
-    return n;
+    return n[k];
+}
+
+// opt in to `bytes` of dynamic shared memory for `kern` once per device
+template <typename F>
+static int ensure_smem(F kern, int bytes, unsigned long long *done, const char *what) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (*done & bit) return 0;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return set_error(e, what);
+    *done |= bit;
+    return 0;
 }
 
 using PrimalLayout = TileLayout<MQ_ETILE, MQ_TILE_ROWS>;
 constexpr int kPrimalSmem = MQ_STAGES * PrimalLayout::kStage + 6 * MQ_STAGES * 8 + MQ_STAGES * 4;
 
+template <bool BUILD>
+static int tile_launch(const mq_market *mk, const mq_state *st, int it, double *xprev,
+                       cudaStream_t s) {
+    static unsigned long long configured = 0;
+    auto kern = primal_fused_kernel<MQ_G, MQ_NSW, MQ_ETILE, MQ_TILE_ROWS, MQ_STAGES, BUILD>;
+    if (int rc = ensure_smem(kern, kPrimalSmem, &configured, "mq_primal_step: smem attribute"))
+        return rc;
+    // the dynamic tile counter lives in blk_done[0]
+    kern<<<mk->prim_grid, (MQ_NSW + 1) * 32, kPrimalSmem, s>>>(*mk, *st, it, xprev, 0, mk->ntiles,
+                                                               st->blk_done);
+    return 0;
+}
+
 int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev, cudaStream_t s) {
-    static bool configured = false;
-    auto kern = primal_fused_kernel<MQ_G, MQ_NSW, MQ_ETILE, MQ_TILE_ROWS, MQ_STAGES>;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kPrimalSmem);
-        if (e != cudaSuccess) return set_error(e, "mq_primal_step: smem attribute");
-        configured = true;
-    }
+    int rc = 0;
     // every dynamic work counter (tiles, long rows, medium rows, full-solve
-    // list and its claims) restarts at 0
-    cudaMemsetAsync(st->blk_done, 0, 5 * sizeof(int32_t), s);
-    if (st->ws_len) {  // screened solve over working sets, then the full-solve list
-        ws_kernel<<<sm_count() * MQ_WS_MINB, 256, 0, s>>>(*mk, *st, it, xprev != nullptr);
-        ws_full_kernel<<<sm_count() * 3, 256, 0, s>>>(*mk, *st, it, xprev);
-    } else if (mk->ntiles > 0) {  // the dynamic tile counter lives in blk_done[0]
-        kern<<<mk->prim_grid, (MQ_NSW + 1) * 32, kPrimalSmem, s>>>(*mk, *st, it, xprev, 0,
-                                                                   mk->ntiles, st->blk_done);
+    // list and its claims, screened batches) restarts at 0
+    cudaMemsetAsync(st->blk_done, 0, 6 * sizeof(int32_t), s);
+    if (st->ws_hdr && !st->ws_rebuild) {  // screened solve, then the full-solve list
+        static unsigned long long wconfigured = 0;
+        if (int rc2 = ensure_smem(ws_kernel, kWsSmem, &wconfigured,
+                                  "mq_primal_step: ws smem attribute"))
+            return rc2;
+        ws_kernel<<<sm_count(), (MQ_WS_NC + 1) * 32, kWsSmem, s>>>(*mk, *st, it,
+                                                                   xprev != nullptr);
+        ws_full_kernel<<<sm_count() * MQ_WSF_MINB, 256, 0, s>>>(*mk, *st, it, xprev);
+    } else if (mk->ntiles > 0) {
+        rc = (st->ws_hdr && st->ws_rebuild) ? tile_launch<true>(mk, st, it, xprev, s)
+                                            : tile_launch<false>(mk, st, it, xprev, s);
+        if (rc) return rc;
     }
     if (mk->nlong > 0) {
         using LS = LongSmem<MQ_LONG_THREADS, MQ_LONG_CAP>;
         auto lk = primal_long_kernel<MQ_LONG_THREADS, MQ_LONG_CAP>;
-        static bool lconfigured = false;
-        if (!lconfigured) {
-            cudaError_t e =
-                cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, LS::kBytes);
-            if (e != cudaSuccess) return set_error(e, "mq_primal_step: long-row smem attribute");
-            lconfigured = true;
-        }
+        static unsigned long long lconfigured = 0;
+        if (int rc2 = ensure_smem(lk, LS::kBytes, &lconfigured,
+                                  "mq_primal_step: long-row smem attribute"))
+            return rc2;
         const int per_sm = MQ_LONG_PER_SM;
         const int grid = grid_for(mk->nlong, 1, sm_count() * per_sm);
         lk<<<grid, MQ_LONG_THREADS, LS::kBytes, s>>>(*mk, *st, it, xprev);
@@ -1412,7 +1652,7 @@ extern "C" {
 
 int mq_dual_step(const mq_market *mk, const mq_state *st, int it, void *stream) {
     return launch_dual(mk, st->p, st->pbar, st->cs, st->cs_prev, st->steps, st->navg, it,
-                       (cudaStream_t)stream, st->ws_len ? st->drift : nullptr);
+                       (cudaStream_t)stream, st->ws_hdr ? st->drift : nullptr);
 }
 
 int mq_primal_step(const mq_market *mk, const mq_state *st, int it, double *x_prev_out,
@@ -1424,7 +1664,7 @@ int mq_primal_step(const mq_market *mk, const mq_state *st, int it, double *x_pr
 int mq_colsum_step(const mq_market *mk, const mq_state *st, int it, int finalize, void *stream) {
     return launch_cs_from_fixed(mk, reinterpret_cast<unsigned long long *>(st->bucket), st->cs,
                                 finalize ? st->csbar : nullptr, st->navg, it,
-                                (cudaStream_t)stream, st->ws_len ? st->drift : nullptr);
+                                (cudaStream_t)stream, st->ws_hdr ? st->drift : nullptr);
 }
 
 int mq_colsum_finalize(const mq_market *mk, const mq_state *st, int it, void *stream) {

@@ -9,15 +9,17 @@
 
 namespace mq {
 
-int sm_count_reduce() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+int sm_count_reduce() {  // per device (a process may use several GPUs)
+    static int n[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int k = dev & 63;
+    if (!n[k]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        n[k] = v > 0 ? v : 148;
     }
-    return n;
+    return n[k];
 }
 
 // scratch layout (doubles)

@@ -48,6 +48,8 @@ class SolveConfig:
     device: object = None              # torch device / index; default current CUDA device
     use_graphs: bool = True            # CUDA-graph capture of chunks
     working_set: bool = True           # screened row solves (exact)
+    group: object = None               # torch.distributed group: buyers row-sharded over
+                                       # its ranks (one GPU each), NCCL all-reduces
 
     def __post_init__(self):
         if self.tol <= 0:
@@ -78,6 +80,7 @@ class SolveConfig:
             "check_every": self.check_every, "threads": self.threads,
             "beta_sufficient": rp.beta_sufficient, "beta_necessary": rp.beta_necessary,
             "beta_artificial": rp.beta_artificial, "row_solver": self.row_solver,
+            **({} if self.group is None else {"ranks": _world(self.group)}),
         }
 
 
@@ -139,8 +142,24 @@ class DeviceSession:
         self.op_norm = selector_norm_from_counts(counts)
 
 
+def _world(group):
+    import torch.distributed as dist
+
+    return dist.get_world_size(group)
+
+
+def split_rows(row_offsets, world):
+    """Contiguous buyer ranges balanced by entries: rank r owns rows
+    [cuts[r], cuts[r+1]) (the partition of bench.shard_rows)."""
+    ro = np.asarray(row_offsets, dtype=np.int64)
+    n, nnz = len(ro) - 1, int(ro[-1])
+    targets = [nnz * r // world for r in range(1, world)]
+    cuts = [0] + [min(n, int(np.searchsorted(ro[1:], t)) + 1) for t in targets] + [n]
+    return [min(c, n) for c in cuts]
+
+
 def solve_on_device(session, cfg, warm_start=None, w_sum=None, inst=None, algo="pdhcg",
-                    fingerprint=None):
+                    fingerprint=None, gather=False):
     """The restarted loop of driver.py:271-377 against a DeviceSession."""
     eng = session.engine
     if fingerprint is None:
@@ -148,9 +167,14 @@ def solve_on_device(session, cfg, warm_start=None, w_sum=None, inst=None, algo="
     if algo == "pdhg":
         warm_start = None  # the lifted solver ignores warm starts (driver.py:271-276)
     if warm_start is not None:
-        x = np.asarray(warm_start["x"], dtype=np.float64)
-        p = np.asarray(warm_start["p"], dtype=np.float64)
-        if x.shape != (session.dm.nnz,) or p.shape != (session.dm.m,):
+        import torch
+
+        x, p = warm_start["x"], warm_start["p"]
+        if not isinstance(x, torch.Tensor):  # device tensors stay on the device
+            x = np.asarray(x, dtype=np.float64)
+        if not isinstance(p, torch.Tensor):
+            p = np.asarray(p, dtype=np.float64)
+        if tuple(x.shape) != (session.dm.nnz,) or tuple(p.shape) != (session.dm.m,):
             raise ValueError("warm start shapes do not match the instance")
         eng.load_state(x, p)
     else:
@@ -222,7 +246,7 @@ def solve_on_device(session, cfg, warm_start=None, w_sum=None, inst=None, algo="
     wall = time.perf_counter() - t0
     log.info("%s finished: status=%s iters=%d restarts=%d rel_kkt=%.3g (%.2fs)", algo, status,
              total, restarts, final.rel_kkt, wall)
-    payload = eng.final_payload()
+    payload = eng.final_payload(gather=gather)
     echo = cfg.as_dict()
     echo["algo"] = algo
     objective = payload.pop("objective")
@@ -244,9 +268,24 @@ def run_solve(inst, cfg, algo, warm_start=None):
     `warm_start`, when given, is a dict {"x": entry-aligned allocation,
     "p": prices} used by the compact solver; algo="pdhg" (lifted PDHG)
     ignores it, as the reference does.
+
+    With cfg.group (a torch.distributed group of N > 1 ranks, one GPU each,
+    every rank calling run_solve), buyers are row-sharded: `inst` is either
+    the whole FisherInstance on every rank (each rank uploads its
+    entry-balanced rows; the report carries the whole allocation) or this
+    rank's FisherShard (the report carries this rank's rows).
     """
     if algo not in ("pdhcg", "pdhg"):
         raise ValueError(f"unknown algorithm {algo!r}")
+    from .instance import FisherShard
+
+    world = 1 if cfg.group is None else _world(cfg.group)
+    if isinstance(inst, FisherShard) or world > 1:
+        if not isinstance(inst, (FisherInstance, FisherShard)):
+            raise TypeError(f"unsupported instance type {type(inst)!r}")
+        if cfg.group is None:
+            raise ValueError("a FisherShard is solved with SolveConfig.group set")
+        return _run_solve_sharded(inst, cfg, algo, warm_start, world)
     if not isinstance(inst, FisherInstance):
         raise TypeError(f"unsupported instance type {type(inst)!r}")
     from .device import DeviceMarket
@@ -260,3 +299,55 @@ def run_solve(inst, cfg, algo, warm_start=None):
     return solve_on_device(session, cfg, warm_start=warm_start,
                            w_sum=float(np.sum(inst.budgets)), inst=inst, fingerprint=fp,
                            algo=algo)
+
+
+def _run_solve_sharded(inst, cfg, algo, warm_start, world):
+    """run_solve on this rank's rows (see run_solve)."""
+    import torch
+    import torch.distributed as dist
+
+    from .device import DeviceMarket
+    from .instance import FisherShard
+
+    rank = dist.get_rank(cfg.group)
+    dev = cfg.device if cfg.device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    u = inst.utilities
+    if isinstance(inst, FisherShard):
+        lo, rows = inst.row_begin, inst.n_buyers
+        e_lo, e_hi = 0, u.nnz
+        rp, col, val, w = u.row_offsets, u.col_indices, u.values, inst.budgets
+        fp = _Fingerprint(None)
+        gather = False
+    else:
+        cuts = split_rows(u.row_offsets, world)
+        lo, hi = cuts[rank], cuts[rank + 1]
+        rows = hi - lo
+        e_lo, e_hi = int(u.row_offsets[lo]), int(u.row_offsets[hi])
+        rp = u.row_offsets[lo:hi + 1] - e_lo
+        col, val, w = u.col_indices[e_lo:e_hi], u.values[e_lo:e_hi], inst.budgets[lo:hi]
+        fp = _Fingerprint(inst)
+        gather = True
+    dm = DeviceMarket(rp, col, val, w, u.n_cols, device=dev, row_begin=lo)
+    # validate() across the ranks: empty rows / budgets locally, goods globally
+    lens = dm.row_ptr[1:] - dm.row_ptr[:-1]
+    bad = [f"buyer {lo + int(i)} values no good" for i in torch.nonzero(lens == 0).flatten()]
+    bad += [f"nonpositive budget for buyer {lo + int(i)}"
+            for i in torch.nonzero(dm.w <= 0).flatten()]
+    counts = dm.col_counts.clone()
+    dist.all_reduce(counts, group=cfg.group)
+    bad += [f"good {int(j)} unvalued" for j in torch.nonzero(counts == 0).flatten()]
+    nbad = torch.tensor([len(bad)], dtype=torch.int64, device=dm.device)
+    dist.all_reduce(nbad, group=cfg.group)
+    if int(nbad.item()):
+        raise ValidationError("; ".join(bad) if bad else "invalid rows on another rank")
+    wsum = torch.tensor([float(np.sum(w))], dtype=torch.float64, device=dm.device)
+    dist.all_reduce(wsum, group=cfg.group)
+    local_warm = None
+    if warm_start is not None and algo == "pdhcg":
+        x = np.asarray(warm_start["x"], dtype=np.float64)
+        local_warm = {"x": x if isinstance(inst, FisherShard) else x[e_lo:e_hi],
+                      "p": warm_start["p"]}
+    session = DeviceSession(None, cfg, group=cfg.group, dm=dm, algo=algo)
+    return solve_on_device(session, cfg, warm_start=local_warm, w_sum=float(wsum.item()),
+                           inst=None, fingerprint=fp, algo=algo, gather=gather)

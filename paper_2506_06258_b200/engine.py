@@ -17,6 +17,7 @@ scalars per check.
 """
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -93,6 +94,22 @@ def to_device(a, device):
 _POOL = None
 
 
+def gather_rows(t, group, world):
+    """Concatenation of every rank's `t` in rank order (all-gather of
+    variable-length row shards, padded to the longest)."""
+    import torch.distributed as dist
+
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(v.item()) for v in sizes]
+    buf = torch.zeros(max(sizes), dtype=t.dtype, device=t.device)
+    buf[:t.numel()] = t
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([p[:k] for p, k in zip(parts, sizes)])
+
+
 def _pcopy(dst, src, piece=1 << 21):
     """np.copyto over threads (numpy drops the GIL; first-touch page faults
     of a fresh output array dominate a single-threaded copy)."""
@@ -126,8 +143,9 @@ class NativeOps:
         self._c(self.lib.mq_dual_step(self.dm.struct, self.eng.state, it, _cur_stream()),
                 "mq_dual_step")
 
-    def primal(self, it):
-        self._c(self.lib.mq_primal_step(self.dm.struct, self.eng.state, it, None, _cur_stream()),
+    def primal(self, it, rebuild=False):
+        st = self.eng.state_rebuild if rebuild else self.eng.state
+        self._c(self.lib.mq_primal_step(self.dm.struct, st, it, None, _cur_stream()),
                 "mq_primal_step")
 
     def colsum_rest(self, it, finalize):
@@ -180,24 +198,37 @@ class NativeOps:
 
 class PdhcgEngine:
     def __init__(self, dm, row_solver="exact", sections=32, subproblem_tol=1e-10,
-                 use_graphs=True, group=None, ops_factory=None, working_set=True):
+                 use_graphs=True, group=None, ops_factory=None, working_set=True,
+                 force_collectives=False, colsum_fp64=False):
         if row_solver not in ("exact", "ksection"):
             raise ValueError("row_solver must be 'exact' or 'ksection'")
         self.dm = dm
         self.mode = row_solver
+        # validation mode: the price step's column sums recomputed in fp64 in
+        # the reference's ascending-row order (mq_colsum) instead of the
+        # fixed-point atomics (tests/test_gpu_baseline_markets.py)
+        self.colsum_fp64 = bool(colsum_fp64)
         self.sections = int(sections)
         self.subtol = float(subproblem_tol)
         self.group = group
         self.world = 1
+        backend = None
         if group is not None:
             import torch.distributed as dist
 
             self.world = dist.get_world_size(group)
-        if self.mode == "ksection" and self.world > 1:
+            backend = dist.get_backend(group)
+        # the N-rank step (collectives between the kernels); force_collectives
+        # runs it on one rank too (tests of the captured collectives on 1 GPU)
+        self.distributed = self.world > 1 or (bool(force_collectives) and group is not None)
+        if self.mode == "ksection" and self.distributed:
             raise ValueError("the k-section drop-in runs on a single GPU")
         self.ops = (ops_factory or NativeOps)(dm, self)
-        self.use_graphs = (bool(use_graphs) and self.world == 1
-                           and getattr(self.ops, "supports_graphs", False))
+        # N ranks: the chunk graph captures the NCCL all-reduces with the
+        # kernels (gloo collectives are host-side and cannot be captured)
+        self.use_graphs = (bool(use_graphs) and getattr(self.ops, "supports_graphs", False)
+                           and (not self.distributed or backend == "nccl")
+                           and os.environ.get("MQ_GRAPH_COLLECTIVES", "1") != "0")
         dev = dm.device
         f64 = dict(dtype=torch.float64, device=dev)
         nnz, m = dm.nnz, dm.m
@@ -229,10 +260,18 @@ class PdhcgEngine:
             self.ws_init = torch.where(lens > int(dm.lib.mq_reg_row()), -3, -1).to(torch.int32)
             if dm.long_rows.numel():
                 self.ws_init[dm.long_rows.to(torch.int64)] = -3
-            self.ws_len = self.ws_init.clone()
-            self.ws_cert = torch.zeros(4 * max(1, dm.n), **f64)
-            self.ws_ux = torch.zeros(2 * K * max(1, dm.n), **f64)
-            self.ws_cp = torch.zeros(2 * K * max(1, dm.n), dtype=torch.int32, device=dev)
+            npad = -(-max(1, dm.n) // 32) * 32
+            # per row (h, theta, P, C): h in ws_len (a view), the rest float bits
+            self.ws_hdr = torch.zeros(npad, 4, dtype=torch.int32, device=dev)
+            self.ws_hdr[:, 0] = -3
+            self.ws_len = self.ws_hdr[:dm.n, 0]
+            self.ws_len.copy_(self.ws_init)
+            self.ws_kmax = torch.zeros(npad // 32, dtype=torch.int32, device=dev)
+            ns = npad * K  # slot k of row i: ((i/32)K + k)32 + i%32
+            self.ws_u = torch.zeros(ns, **f64)
+            self.ws_x = torch.zeros(ns, **f64)
+            self.ws_col = torch.zeros(ns, dtype=torch.int32, device=dev)
+            self.ws_pos = torch.zeros(ns, dtype=torch.uint8, device=dev)
             self.ws_list = torch.zeros(max(1, dm.n), dtype=torch.int32, device=dev)
             self.drift = torch.zeros(2, **f64)
         # fixed-point column sums: m u64 accumulators, zero between iterations
@@ -265,7 +304,7 @@ class PdhcgEngine:
         self.navg = 0
         self.tau = self.sigma = None
         self._graphs = {}
-        if self.fixed and self.world > 1:
+        if self.fixed and self.distributed:
             # one fixed-point scale on every rank (from the global column
             # counts), so the ranks' integer column sums add exactly: the
             # all-reduce runs on the u64 accumulators and the N-rank column
@@ -275,6 +314,13 @@ class PdhcgEngine:
             gmax = int(self._global_counts().max().item()) if m else 1
             dm.struct.cs_scale, dm.struct.cs_xmax = fixed_point_scale(gmax)
         self.state = self._make_state()
+        # the same state with ws_rebuild set: the tile kernel rebuilds every
+        # working set (first iteration after the host wrote x or p)
+        self.state_rebuild = None
+        if self.state is not None and self.working_set:
+            self.state_rebuild = self._make_state()
+            self.state_rebuild.ws_rebuild = 1
+        self._rebuild = True
 
     # ------------------------------------------------------------ plumbing
     def _make_state(self):
@@ -285,14 +331,15 @@ class PdhcgEngine:
                      "steps", "faults", "srow", "bucket", "xflag", "xsum"):
             setattr(s, name, getattr(self, name).data_ptr())
         if self.working_set:
-            for name in ("ws_len", "ws_cert", "ws_ux", "ws_cp", "ws_list", "drift"):
+            for name in ("ws_hdr", "ws_kmax", "ws_u", "ws_x", "ws_col", "ws_pos", "ws_list",
+                         "drift"):
                 setattr(s, name, getattr(self, name).data_ptr())
         s.navg = self.navg_dev.data_ptr()
         s.pass_out = self.pass_buf.data_ptr()
         return s
 
     def _allreduce(self, t, op="sum"):
-        if self.world > 1:
+        if self.distributed:
             import torch.distributed as dist
 
             red = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX,
@@ -310,6 +357,8 @@ class PdhcgEngine:
         running sum restarts from navg * xbar and no working set is valid."""
         if self.working_set:
             self.ws_len.copy_(self.ws_init)
+            self.ws_kmax.zero_()
+            self._rebuild = True
         if self.sparse:
             self.xflag.fill_(1)
             if self.navg:
@@ -398,6 +447,8 @@ class PdhcgEngine:
             self.xflag.fill_(1)
         if self.working_set:
             self.ws_len.copy_(self.ws_init)
+            self.ws_kmax.zero_()
+            self._rebuild = True
 
     # ------------------------------------------------------------ chunks
     def run_chunk(self, iters):
@@ -407,13 +458,27 @@ class PdhcgEngine:
             return self._run_chunk_ksection(iters)
         if iters > self.pass_buf.numel():
             raise ValueError("chunk longer than the pass buffer")
+        rebuild = self.working_set and self._rebuild
         if self.use_graphs:
-            g = self._graphs.get(iters)
+            g = self._graphs.get((iters, rebuild))
             if g is None:
-                g = self._capture(iters)
-            g.replay()
+                try:
+                    g = self._capture(iters, rebuild)
+                except Exception as exc:  # capture unsupported: eager launches
+                    if not self.distributed:
+                        raise
+                    import warnings
+
+                    warnings.warn(f"chunk capture with collectives failed ({exc}); "
+                                  "launching eagerly")
+                    self.use_graphs = False
+            if g is not None:
+                g.replay()
+            else:
+                self._launch_chunk(iters, rebuild)
         else:
-            self._launch_chunk(iters)
+            self._launch_chunk(iters, rebuild)
+        self._rebuild = False
         self.navg += iters
         vals = torch.cat([self.pass_buf[:iters], self.faults]).cpu().numpy()
         if vals[-1]:
@@ -424,21 +489,27 @@ class PdhcgEngine:
             raise SubproblemError(f"{int(vals[-2])} row subproblems failed to converge")
         return [int(v) for v in vals[:-2]]
 
-    def _launch_chunk(self, iters):
+    def _launch_chunk(self, iters, rebuild=False):
         """One chunk: per iteration price step, fused prox + column sums, and on
         N ranks the all-reduce of the m-length column sums before the running
-        average of colsum(xbar) is updated."""
+        average of colsum(xbar) is updated.  rebuild: the first iteration
+        rebuilds every working set (after the host invalidated them)."""
         ops = self.ops
         self.pass_buf[:iters].zero_()
         self.faults.zero_()
-        single = self.world == 1
+        single = not self.distributed
         exact = self.fixed and not single
         for it in range(iters):
             ops.dual(it)
-            ops.primal(it)
+            ops.primal(it, rebuild=rebuild and it == 0)
             if exact:  # integer all-reduce of the fixed-point sums, then convert
                 self._allreduce(self.bucket.view(torch.int64)[:self.dm.m])
                 ops.colsum_rest(it, True)
+                continue
+            if self.colsum_fp64 and single:
+                ops.colsum_rest(it, False)  # zeroes the accumulators, advances the drift
+                ops.colsum(self.x, self.cs)
+                ops.finalize(it)
                 continue
             ops.colsum_rest(it, single)
             if not single:
@@ -449,16 +520,16 @@ class PdhcgEngine:
             self._allreduce(self.faults)
         ops.chunk_end(iters)
 
-    def _capture(self, iters):
+    def _capture(self, iters, rebuild=False):
         g = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream(device=self.dm.device)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
             torch.cuda.synchronize(self.dm.device)
         with torch.cuda.graph(g, stream=side):
-            self._launch_chunk(iters)
+            self._launch_chunk(iters, rebuild)
         torch.cuda.current_stream().wait_stream(side)
-        self._graphs[iters] = g
+        self._graphs[(iters, rebuild)] = g
         return g
 
     def _run_chunk_ksection(self, iters):
@@ -478,7 +549,7 @@ class PdhcgEngine:
         self.colbest[k].zero_()
         self.ops.resid_rows(x, p, use_norm, self.colbest[k], t_out, self.out[16 * k: 16 * k + 8],
                             self.scratch if k == 0 else self.scratch2)
-        if self.world > 1:
+        if self.distributed:
             o = self.out[16 * k: 16 * k + 8]
             self._allreduce(self.colbest[k], "max")
             mx = o[0:4].clone()
@@ -538,21 +609,29 @@ class PdhcgEngine:
         o = self.out[24:28]
         self.ops.restart_moves(self.xbar, self.x0, self.pbar, self.p0, self.csbar, self.cs0, o,
                                self.scratch)
-        if self.world > 1:
+        if self.distributed:
             sx = o[0:1].clone()
             self._allreduce(sx, "sum")
             o[0:1].copy_(sx)
         dxx, dpp, inter = (float(v) for v in o[0:3].cpu().numpy())
         return math.sqrt(dxx), math.sqrt(dpp), dxx, dpp, abs(inter)
 
-    def final_payload(self):
-        """prices, allocation, utility values, dual values, objective."""
+    def _gather(self, t):
+        return gather_rows(t, self.group, self.world)
+
+    def final_payload(self, gather=False):
+        """prices, allocation, utility values, dual values, objective.  On N
+        ranks the allocation and the per-buyer values are this rank's rows,
+        or (gather=True) the whole market's in row order."""
         self._rows(self.x, self.p, 0, 0, t_out=self.t_buf)
         v = self.out[0:8].cpu().numpy()
-        t = self.t_buf.cpu().numpy()
-        w = self.dm.w.cpu().numpy()
+        x, t, w = self.x, self.t_buf, self.dm.w
+        if gather and self.world > 1:
+            x, t, w = self._gather(x), self._gather(t), self._gather(w)
+        t = t.cpu().numpy()
+        w = w.cpu().numpy()
         with np.errstate(divide="ignore"):
             y = w / t
         obj = -float(v[5]) if v[6] == 0 else math.inf
-        return {"prices": self.p.cpu().numpy(), "allocation": to_host(self.x),
+        return {"prices": self.p.cpu().numpy(), "allocation": to_host(x),
                 "utility_values": t, "dual_values": y, "objective": obj}

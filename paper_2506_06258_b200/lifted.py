@@ -294,8 +294,9 @@ class LiftedEngine:
             torch.div(out_y, sig, out=vt)
         return math.sqrt(sig)
 
-    def final_payload(self):
-        """prices, allocation, t and y on the original instance, objective."""
+    def final_payload(self, gather=False):
+        """prices, allocation, t and y on the original instance, objective
+        (gather=True on N ranks: the whole market's rows, in row order)."""
         ux = torch.zeros(self.dm.n, dtype=torch.float64, device=self.dm.device)
         self.row_dot(self.x, ux, use_norm=0)
         if bool((ux <= 0).any().item()):
@@ -304,6 +305,11 @@ class LiftedEngine:
             part = -(self.dm.w * torch.log(ux)).sum().reshape(1)
             obj = float(self._allreduce(part).item())
         scales = self.dm.scales
-        return {"prices": self.p.cpu().numpy(), "allocation": to_host(self.x),
-                "utility_values": (self.t * scales).cpu().numpy(),
-                "dual_values": (self.y / scales).cpu().numpy(), "objective": obj}
+        x, t, y = self.x, self.t * scales, self.y / scales
+        if gather and self.world > 1:
+            from .engine import gather_rows
+
+            x, t, y = (gather_rows(v, self.group, self.world) for v in (x, t, y))
+        return {"prices": self.p.cpu().numpy(), "allocation": to_host(x),
+                "utility_values": t.cpu().numpy(), "dual_values": y.cpu().numpy(),
+                "objective": obj}

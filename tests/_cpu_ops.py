@@ -64,7 +64,7 @@ class OracleOps:
         e.pbar.copy_(wold * e.pbar + wnew * e.p)
         e.cs_prev.copy_(e.cs)
 
-    def primal(self, it):
+    def primal(self, it, rebuild=False):
         e, dm = self.e, self.dm
         wold, wnew = self._avg(it)
         tau = float(e.steps[0])

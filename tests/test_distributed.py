@@ -152,3 +152,112 @@ def test_two_rank_device_solve_matches_single_rank(name, tmp_path):
         assert rel_max(r[k]["prices"], one.prices) <= 1e-9
     alloc = np.concatenate([r[0]["allocation"], r[1]["allocation"]])
     assert np.allclose(alloc, one.allocation, rtol=1e-8, atol=1e-12)
+
+
+def _api_worker(rank, world, port, name, out_dir, mode):
+    """One rank calling the public run_solve with SolveConfig(group=...):
+    mode "full" passes the whole instance (the solver takes its rows and
+    gathers the allocation), "shard" passes this rank's FisherShard."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(__file__))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(__file__)))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2506_06258_b200 as mq
+    from paper_2506_06258_b200.driver import split_rows
+
+    g = golden(name)
+    inst = instance_from(g)
+    cfg = _cfg(g).with_overrides(group=dist.group.WORLD)
+    if mode == "shard":
+        u = inst.utilities
+        cuts = split_rows(u.row_offsets, world)
+        lo, hi = cuts[rank], cuts[rank + 1]
+        e0, e1 = int(u.row_offsets[lo]), int(u.row_offsets[hi])
+        sm = mq.SparseMatrix(hi - lo, u.n_cols, u.row_offsets[lo:hi + 1] - e0,
+                             u.col_indices[e0:e1], u.values[e0:e1])
+        inst = mq.FisherShard(sm, inst.budgets[lo:hi], lo, u.n_rows)
+    rep = mq.run_solve(inst, cfg, "pdhcg")
+    np.savez(os.path.join(out_dir, f"api{rank}.npz"), prices=rep.prices,
+             allocation=rep.allocation, t=rep.utility_values, iters=rep.inner_iterations,
+             restarts=rep.restarts, objective=rep.objective, fp=rep.instance_fingerprint)
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["full", "shard"])
+def test_run_solve_with_a_group_matches_single_rank(mode, tmp_path):
+    import paper_2506_06258_b200 as mq
+
+    name = "solve_g200_tol0.npz"
+    g = golden(name)
+    inst = instance_from(g)
+    one = mq.run_solve(inst, _cfg(g), "pdhcg")
+    mp.start_processes(_api_worker, args=(2, _free_port(), name, str(tmp_path), mode), nprocs=2,
+                       start_method="spawn")
+    r = [np.load(tmp_path / f"api{k}.npz") for k in range(2)]
+    for k in range(2):
+        assert int(r[k]["iters"]) == one.inner_iterations == int(g["iters"])
+        assert int(r[k]["restarts"]) == one.restarts == int(g["restarts"])
+        assert rel_max(r[k]["prices"], one.prices) <= 1e-9
+        assert abs(float(r[k]["objective"]) / one.objective - 1.0) <= 1e-8
+    if mode == "full":  # every rank reports the whole market
+        for k in range(2):
+            assert np.allclose(r[k]["allocation"], one.allocation, rtol=1e-8, atol=1e-12)
+            assert np.allclose(r[k]["t"], one.utility_values, rtol=1e-9)
+            assert str(r[k]["fp"]) == one.instance_fingerprint
+    else:
+        alloc = np.concatenate([r[0]["allocation"], r[1]["allocation"]])
+        assert np.allclose(alloc, one.allocation, rtol=1e-8, atol=1e-12)
+
+
+def _nccl_capture_worker(rank, world, port, name, out_dir):
+    """A 1-rank NCCL group with the N-rank step forced: the chunk graph
+    captures the NCCL all-reduce of the fixed-point column sums together with
+    the kernels (what N GPUs replay every chunk)."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(__file__))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(__file__)))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", 0))
+    from paper_2506_06258_b200.device import DeviceMarket
+    from paper_2506_06258_b200.engine import PdhcgEngine
+
+    g = golden(name)
+    inst = instance_from(g)
+    out = {}
+    for tag, force in (("forced", True), ("plain", False)):
+        dm = DeviceMarket.from_instance(inst)
+        eng = PdhcgEngine(dm, group=dist.group.WORLD, force_collectives=force)
+        eng.initial_state()
+        eng.set_steps(0.05, 0.05)
+        for _ in range(3):
+            eng.run_chunk(40)
+        torch.cuda.synchronize()
+        out[tag + "_p"] = eng.p.cpu().numpy()
+        out[tag + "_x"] = eng.x.cpu().numpy()
+        out[tag + "_graphs"] = np.array([eng.use_graphs, len(eng._graphs) > 0, eng.distributed])
+    np.savez(os.path.join(out_dir, "nccl.npz"), **out)
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_collectives_are_captured_in_the_chunk_graph(tmp_path):
+    mp.start_processes(_nccl_capture_worker,
+                       args=(1, _free_port(), "solve_g200_tol0.npz", str(tmp_path)), nprocs=1,
+                       start_method="spawn")
+    r = np.load(tmp_path / "nccl.npz")
+    assert list(r["forced_graphs"]) == [1, 1, 1]   # captured with the collectives
+    assert list(r["plain_graphs"]) == [1, 1, 0]
+    # integer all-reduce of one rank is the identity: bitwise the same iterate
+    assert np.array_equal(r["forced_p"], r["plain_p"])
+    assert np.array_equal(r["forced_x"], r["plain_x"])

@@ -93,17 +93,21 @@ def test_working_set_slots_mirror_the_iterate():
     h = ws.ws_len.cpu().numpy()
     rp = ws.dm.row_ptr.cpu().numpy()
     u, x, col = ws.dm.u.cpu().numpy(), ws.x.cpu().numpy(), ws.dm.col.cpu().numpy()
-    ux = ws.ws_ux.cpu().numpy().reshape(-1, K, 2)
-    cp = ws.ws_cp.cpu().numpy().reshape(-1, K, 2)
+
+    def slots(t):  # [n/32, K, 32] -> [n, K]
+        a = t.cpu().numpy().reshape(-1, K, 32)
+        return a.transpose(0, 2, 1).reshape(-1, K)
+
+    su, sx, sc, sp = slots(ws.ws_u), slots(ws.ws_x), slots(ws.ws_col), slots(ws.ws_pos)
     rows = np.nonzero(h >= 0)[0]
     assert len(rows) > 0.9 * len(h)
     for i in rows[:: max(1, len(rows) // 500)]:
         k = h[i]
-        pos = cp[i, :k, 1]
+        pos = sp[i, :k].astype(np.int64)
         assert np.all(np.diff(pos) > 0)
         g = rp[i] + pos
-        assert np.array_equal(cp[i, :k, 0], col[g])
-        assert np.array_equal(ux[i, :k, 0], u[g]) and np.array_equal(ux[i, :k, 1], x[g])
+        assert np.array_equal(sc[i, :k], col[g])
+        assert np.array_equal(su[i, :k], u[g]) and np.array_equal(sx[i, :k], x[g])
         nz = np.nonzero(x[rp[i]:rp[i + 1]] > 0)[0]
         assert set(nz.tolist()) <= set(pos.tolist())
 
