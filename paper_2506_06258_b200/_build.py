@@ -6,6 +6,7 @@ The k-section drop-in (ksection.cu) is compiled with --fmad=false so its
 arithmetic rounds exactly like the reference's; the fast path may contract.
 """
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -32,21 +33,42 @@ SOURCES = {
 }
 
 
-def _sources_newer_than_lib():
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    deps.append(os.path.join(INCLUDE, "market_eq_b200.h"))
-    return any(os.path.getmtime(d) > t for d in deps)
+def source_digest(extra_flags=()):
+    """SHA-256 of everything the library is built from: every file of csrc/,
+    the public header, the compiler and the flags.  Stored next to the
+    library (`<lib>.sha256`) by build(); a prebuilt library is trusted only
+    when its digest matches the sources it ships with (not their mtimes)."""
+    h = hashlib.sha256()
+    for name in sorted(os.listdir(CSRC)):
+        path = os.path.join(CSRC, name)
+        if os.path.isfile(path):
+            h.update(name.encode() + b"\0")
+            with open(path, "rb") as fh:
+                h.update(fh.read())
+    with open(os.path.join(INCLUDE, "market_eq_b200.h"), "rb") as fh:
+        h.update(fh.read())
+    h.update(repr((NVCC, ARCH, COMMON, sorted(SOURCES.items()), list(extra_flags))).encode())
+    return h.hexdigest()
+
+
+def _digest_path(lib):
+    return lib + ".sha256"
+
+
+def up_to_date(lib=LIB, extra_flags=()):
+    try:
+        with open(_digest_path(lib)) as fh:
+            return os.path.exists(lib) and fh.read().strip() == source_digest(extra_flags)
+    except OSError:
+        return False
 
 
 def build(force=False, verbose=False, extra_flags=(), out=None):
     target = out or LIB
     if out is None and os.environ.get("MQ_LIB"):
         return os.environ["MQ_LIB"]  # a prebuilt variant was selected
-    if not force and not _sources_newer_than_lib():
-        return LIB
+    if not force and up_to_date(target, extra_flags):
+        return target
     with tempfile.TemporaryDirectory() as tmp:
         objs = []
         for src, extra in SOURCES.items():
@@ -63,6 +85,8 @@ def build(force=False, verbose=False, extra_flags=(), out=None):
                "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         subprocess.run(cmd, check=True)
         os.replace(tmp_lib, target)
+    with open(_digest_path(target), "w") as fh:
+        fh.write(source_digest(extra_flags) + "\n")
     return target
 
 

@@ -7,8 +7,8 @@
     long_rows int32 [nlong]       rows longer than 1024 entries
     med_rows int32 [nmed]         tile rows longer than 128 entries (warp per row)
     bperm    int32 [nnz]          tile-blocked transpose schedule: per block of
-    bptr     int32 [(nblk+1)m+1]  8 x prim_grid tiles, per good, ascending rows
-                                  (pseudo-block nblk = the long rows)
+    bptr     int32 [(nblk+1)m+1]  4 x prim_grid tiles, per good, ascending rows
+                                  (block nblk empty)
     tperm / tptr                  the reference's global schedule (sparse.py:
                                   130-145), only for the k-section drop-in
 (pad) = 16 readable elements past the end for the TMA bulk copies.
@@ -106,7 +106,11 @@ def sm_count(device):
 def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
                            tiles_per_cta=TILES_PER_CTA_PER_BLOCK, tiles_per_block=None):
     """Entry positions grouped by (block of tiles, good), ascending inside a
-    good; long-row entries form the last pseudo-block.  Returns
+    good.  A block covers the entries from its first tile's start to the next
+    block's (long rows between tiles included), so walking a good block by
+    block visits its entries in ascending row order: the reference's
+    column_sums order (np.bincount over storage order, sparse.py:200-210).
+    The last block index nblk is kept (empty) for the layout.  Returns
     (bperm int32 [nnz], bptr int32 [(nblk+1)*m+1], nblk, tiles_per_block)."""
     dev = col.device
     nnz = col.numel()
@@ -116,19 +120,10 @@ def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
     pos = torch.arange(nnz, device=dev, dtype=torch.int64)
     if nblk:
         starts = row_ptr[tiles[::tpb, 0]].contiguous()
-        blk = torch.searchsorted(starts, pos, right=True) - 1
+        blk = (torch.searchsorted(starts, pos, right=True) - 1).clamp_(min=0)
     else:
         blk = torch.zeros(nnz, dtype=torch.int64, device=dev)
     del pos
-    if long_rows.numel():
-        lr = long_rows.to(torch.int64)
-        d = torch.zeros(nnz + 1, dtype=torch.int32, device=dev)
-        d.index_add_(0, row_ptr[lr], torch.ones_like(lr, dtype=torch.int32))
-        d.index_add_(0, row_ptr[lr + 1], -torch.ones_like(lr, dtype=torch.int32))
-        is_long = torch.cumsum(d, 0, dtype=torch.int32)[:nnz] > 0
-        del d
-        blk = torch.where(is_long, torch.full_like(blk, nblk), blk)
-        del is_long
     total = (nblk + 1) * m
     if total < 2 ** 31:
         key = blk.to(torch.int32) * m + col
@@ -136,7 +131,6 @@ def build_blocked_schedule(row_ptr, col, m, tiles, long_rows, prim_grid,
         key = blk * m + col.to(torch.int64)
     del blk
     _, perm = torch.sort(key, stable=True)
-    # [pad]: the fused kernel stages slices of both arrays with TMA bulk copies
     bperm = torch.zeros(nnz + nat.PAD, dtype=torch.int32, device=dev)
     bperm[:nnz] = perm
     del perm

@@ -259,8 +259,9 @@ def test_tiles_are_greedy_and_medium_rows_listed():
 
 
 def test_blocked_schedule_preserves_column_order():
-    """Walking a good block by block (tiles, then the long-row pseudo-block)
-    visits its tile entries in ascending row order, and every entry once."""
+    """Walking a good block by block visits every entry of the good once, in
+    ascending row order (long rows included where they lie): the reference's
+    column_sums order."""
     import torch
 
     from paper_2506_06258_b200.device import build_blocked_schedule, build_tiles
@@ -268,7 +269,7 @@ def test_blocked_schedule_preserves_column_order():
     rng = np.random.default_rng(1)
     n, m = 700, 60
     lens = rng.poisson(8, n) + 1
-    lens[[5, 300, 301, 650]] = [59, 45, 50, 40]     # long rows (threshold 30 below)
+    lens[[0, 5, 300, 301, 650]] = [35, 59, 45, 50, 40]   # long rows (threshold 30 below)
     rp, col = _random_csr(rng, n, m, lens)
     rpt = torch.from_numpy(rp)
     tiles, long_rows = build_tiles(rpt, 64, 30, 16)
@@ -278,19 +279,11 @@ def test_blocked_schedule_preserves_column_order():
     bperm, bptr = bperm.numpy(), bptr.numpy()
     assert tpb == 6 and nblk == -(-tiles.shape[0] // 6)
     assert np.array_equal(np.sort(bperm), np.arange(len(col)))
-    row_of = np.repeat(np.arange(n), np.diff(rp))
-    is_long = np.isin(row_of, long_rows.numpy())
-    tstart = rp[tiles[:, 0].numpy()]
     for j in range(m):
-        walk = np.concatenate([bperm[bptr[b * m + j]:bptr[b * m + j + 1]] for b in range(nblk)])
-        ref = np.flatnonzero((col == j) & ~is_long)
-        assert np.array_equal(walk, ref)
-        lw = bperm[bptr[nblk * m + j]:bptr[nblk * m + j + 1]]
-        assert np.array_equal(lw, np.flatnonzero((col == j) & is_long))
-        for b in range(nblk):
-            seg = bperm[bptr[b * m + j]:bptr[b * m + j + 1]]
-            blk = np.searchsorted(tstart[::6], seg, side="right") - 1
-            assert np.all(blk == b)
+        walk = np.concatenate([bperm[bptr[b * m + j]:bptr[b * m + j + 1]]
+                               for b in range(nblk + 1)])
+        assert np.array_equal(walk, np.flatnonzero(col == j))
+        assert bptr[nblk * m + j] == bptr[nblk * m + j + 1]   # the last block is empty
 
 
 def test_fixed_point_scale_cannot_overflow():
@@ -308,3 +301,21 @@ def test_fixed_point_scale_cannot_overflow():
         assert xmax * scale * max(1, c) <= 2.0 ** 62 * (1 + 1e-12)
         if c <= 10**6:
             assert xmax >= 1024
+
+
+def test_library_is_verified_by_source_digest(tmp_path):
+    """build() trusts a prebuilt library only if the digest stored beside it
+    matches the sources, header, compiler and flags it would be built from."""
+    import shutil
+
+    from paper_2506_06258_b200 import _build
+
+    d = _build.source_digest()
+    assert d == _build.source_digest() and d != _build.source_digest(("-DMQ_WS_GAMMA=1.1",))
+    lib = tmp_path / "lib.so"
+    shutil.copy(_build.LIB, lib) if os.path.exists(_build.LIB) else lib.write_bytes(b"x")
+    assert not _build.up_to_date(str(lib))              # no digest beside it
+    (tmp_path / "lib.so.sha256").write_text(d + "\n")
+    assert _build.up_to_date(str(lib))
+    (tmp_path / "lib.so.sha256").write_text("0" * 64 + "\n")
+    assert not _build.up_to_date(str(lib))              # stale or foreign build
