@@ -58,3 +58,21 @@ def test_diagnostics_reject_nonpositive_xi():
         mq.scaled_kkt_residual(inst, g["a0_x"], g["a0_t"], g["a0_p"], g["a0_y"], 0.0)
     with pytest.raises(ValueError):
         mq.smoothed_gap(inst, (g["a0_x"], g["a0_p"]), (g["a0_xc"], g["a0_pc"]), xi=-1.0)
+
+
+def test_property_suite_passes():
+    """theory.py's battery (market_eq/theory.py:215-302) on the device paths:
+    boundedness, averaged distance, smoothed-gap nonnegativity, grid
+    agreement, cross-solver prices, relabeling symmetry, exchange decay."""
+    from paper_2506_06258_b200.theory import run_property_suite
+
+    rep = run_property_suite(seed=0)
+    names = {c["name"] for c in rep["checks"]}
+    assert names >= {"iterate-boundedness", "averaged-distance", "smoothed-gap-nonnegative",
+                     "cross-solver-prices", "relabeling-symmetry",
+                     "smoothed-gap-grid-agreement", "exchange-geometric-decay"}
+    for c in rep["checks"]:
+        print(c)
+    assert rep["all_passed"], [c for c in rep["checks"] if not c["passed"]]
+    ran = [c for c in rep["checks"] if not c["skipped"]]
+    assert len(ran) >= 15

@@ -48,13 +48,21 @@ def gb(x, unit):
 
 
 traffic = {}
+# the primal step = every kernel mq_primal_step launches (one launch each in
+# the capture): screened solve + full-solve list + medium / long rows, or the
+# unscreened tile kernel
+PRIMAL = ("ws_kernel", "ws_full_kernel", "primal_med", "primal_long", "primal_fused")
+rd = wr = 0.0
+names = []
 for name, d in out.items():
-    if "primal_fused" in name:
-        rd = gb(*d["dram__bytes_read.sum"])
-        wr = gb(*d["dram__bytes_write.sum"])
-        traffic["primal"] = {"dram_bytes_per_launch": (rd + wr) * 1e9, "read_gb": rd,
-                             "write_gb": wr, "kernel": name, "source": rep,
-                             "config": "c4"}  # tools/measure_round.sh profiles config 4
+    if any(t in name for t in PRIMAL):
+        rd += gb(*d["dram__bytes_read.sum"])
+        wr += gb(*d["dram__bytes_write.sum"])
+        names.append(name.split("(")[0])
+if names:
+    traffic["primal"] = {"dram_bytes_per_launch": (rd + wr) * 1e9, "read_gb": rd,
+                         "write_gb": wr, "kernels": names, "source": rep,
+                         "config": "c4"}
 json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
 # launch list: per-kernel share of device time
 tot = defaultdict(float)
@@ -80,7 +88,8 @@ md += ["", "## Launch list (ncu, cold-cache, serialised)", "", "| kernel | launc
        "|---|---|---|---|"]
 for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
     md.append(f"| {k} | {cnt[k]} | {v:.3f} | {100 * v / S:.1f}% |")
-ITER = ("primal_fused", "dual_kernel", "colsum_finalize", "chunk_end", "colsum_blocks", "primal_long", "primal_med", "cs_from_fixed")
+ITER = ("primal_fused", "ws_kernel", "ws_full_kernel", "dual_kernel", "colsum_finalize",
+        "chunk_end", "primal_long", "primal_med", "cs_from_fixed", "avg_materialize")
 it = {k: v for k, v in tot.items() if any(t in k for t in ITER)}
 SI = sum(it.values()) or 1.0
 md += ["", "## Per-iteration kernels only (the bench's timed region)", "",
