@@ -330,6 +330,8 @@ def main():
         if shared:
             dist.init_process_group("gloo")
         else:
+            # NCCL's INFO lines show the communicator (ranks, NVLink/NVLS paths)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
     if a.impl == "reference":

@@ -235,6 +235,14 @@ int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream);
 int mq_resid_rows(const mq_market *mk, const double *x, const double *p, int use_norm,
                   double *colbest, double *work, double *t_out, double *y_out, double *row_out,
                   double *scratch, void *stream);
+/* Both row passes of a check in one sweep (the fast path's state): the
+ * last iterate (st->x with st->xflag, st->p) and the average (st->xbar,
+ * st->pbar), original utilities; each side exactly as mq_resid_rows with
+ * use_norm = 0 (bitwise the two separate calls).  work: 4m doubles. */
+int mq_resid_rows_pair(const mq_market *mk, const mq_state *st, double *colbest_last,
+                       double *colbest_avg, double *work, double *row_out_last,
+                       double *row_out_avg, double *scratch_last, double *scratch_avg,
+                       void *stream);
 /* Column pass (replicated data): col_out[6] (device):
  * [0] max |cs - 1|, [1] max |cs|, [2] max (colbest - p)_+, [3] max (p - colbest)
  * (initial 0), [4] sum (cs - 1)^2, [5] sum min(p - colbest, 0)^2. */

@@ -82,6 +82,7 @@ _SIGS = {
     "mq_colsum": (CINT, [PM, P, P, P]),
     "mq_resid_rows": (CINT, [PM, P, P, CINT, P, P, P, P, P, P, P]),
     "mq_resid_cols": (CINT, [I64, P, P, P, P, P, P]),
+    "mq_resid_rows_pair": (CINT, [PM, PS, P, P, P, P, P, P, P, P]),
     "mq_restart_moves": (CINT, [PM, P, P, P, P, P, P, P, P, P]),
     "mq_spmv": (CINT, [I64, P, P, P, P, P, P]),
     "mq_normalize_rows": (CINT, [I64, P, P, P, P, P]),

@@ -1362,14 +1362,12 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 if ((wm >> k) & 1u) {
+                    // the slot is authoritative; x and its flag are written
+                    // back once per chunk (ws_flush_kernel)
                     const double xn = fmax(c[k] + tw * u[k] * inv_s, 0.0);
-                    const bool nz = xn > 0.0, wz = (was >> k) & 1u;
-                    const int64_t g = e0 + pos[k];
                     st.ws_x[ws_at(i, k)] = xn;
-                    st.x[g] = xn;
-                    if (nz != wz) st_flag(st.xflag + g, nz);
-                    if (nz) {
-                        red_add_f64(st.xsum + g, xn);
+                    if (xn > 0.0) {
+                        red_add_f64(st.xsum + e0 + pos[k], xn);
                         fixed_colsum_add(mk, st, jc[k], xn);
                     }
                 }
@@ -1421,7 +1419,7 @@ ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict
         }
         double c[RP], u[RP], pv[RP], xv[RP];
         int jc[RP];
-        uint32_t fb = 0;
+        uint32_t fb = 0;  // x > 0 flags as stored
 #pragma unroll
         for (int e = 0; e < RP; ++e) {
             const int t = lane + e * G;
@@ -1430,11 +1428,39 @@ ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict
             u[e] = in ? __ldg(mk.u + a + t) : 0.0;
             if (in && __ldcg(st.xflag + a + t)) fb |= 1u << e;
         }
+        uint32_t was = fb;  // entries whose x^k is nonzero
+        if (hold >= 0) {
+            // a row solved over its working set so far this chunk: x^k lives
+            // in its slots (x and the flags are written back at chunk end);
+            // every other entry of the row is zero
+            was = 0;
 #pragma unroll
-        for (int e = 0; e < RP; ++e) {
-            const int t = lane + e * G;
-            pv[e] = t < len ? __ldg(st.p + jc[e]) : 0.0;
-            xv[e] = ((fb >> e) & 1u) ? __ldcg(st.x + a + t) : 0.0;
+            for (int e = 0; e < RP; ++e) xv[e] = 0.0;
+            for (int k = 0; k < hold; ++k) {
+                const int64_t at = ws_at(i, k);
+                const int ps = __ldcg(st.ws_pos + at);
+                if ((ps & (G - 1)) == lane) {
+                    const double xk = __ldcg(st.ws_x + at);
+#pragma unroll
+                    for (int e = 0; e < RP; ++e)
+                        if (e == (ps >> 4)) {
+                            xv[e] = xk;
+                            if (xk > 0.0) was |= 1u << e;
+                        }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < RP; ++e) {
+                const int t = lane + e * G;
+                pv[e] = t < len ? __ldg(st.p + jc[e]) : 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < RP; ++e) {
+                const int t = lane + e * G;
+                pv[e] = t < len ? __ldg(st.p + jc[e]) : 0.0;
+                xv[e] = ((fb >> e) & 1u) ? __ldcg(st.x + a + t) : 0.0;
+            }
         }
         const double tw = tau * w;
 #pragma unroll
@@ -1453,10 +1479,10 @@ ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict
             const int t = lane + e * G;
             xn[e] = t < len ? fmax(c[e] + tw * u[e] * inv_s, 0.0) : 0.0;
             if (t < len) {
-                const bool nz = xn[e] > 0.0, was = (fb >> e) & 1u;
+                const bool nz = xn[e] > 0.0, fl = (fb >> e) & 1u;
                 const int64_t g = a + t;
-                if (nz != was) st_flag(st.xflag + g, nz);
-                if (nz || was) st.x[g] = xn[e];
+                if (nz != fl) st_flag(st.xflag + g, nz);
+                if (nz || fl || ((was >> e) & 1u)) st.x[g] = xn[e];
                 if (nz) {
                     red_add_f64(st.xsum + g, xn[e]);
                     fixed_colsum_add(mk, st, jc[e], xn[e]);
@@ -1547,6 +1573,24 @@ __global__ void avg_materialize_kernel(int64_t nnz, const double *__restrict__ x
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
          e += (int64_t)gridDim.x * blockDim.x)
         xbar[e] = count > 0.0 ? xsum[e] / count : xbar[e];
+}
+
+// End of a chunk: x and its flags of every row with a working set, from the
+// slots (inside a chunk the screened solve writes only the slots)
+__global__ void ws_flush_kernel(int64_t n, const int64_t *__restrict__ row_ptr, mq_state st) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int h = st.ws_hdr[4 * i];
+        if (h <= 0) continue;
+        const int64_t e0 = row_ptr[i];
+        for (int k = 0; k < h; ++k) {
+            const int64_t at = ws_at(i, k);
+            const int64_t g = e0 + st.ws_pos[at];
+            const double x = st.ws_x[at];
+            st.x[g] = x;
+            st.xflag[g] = x > 0.0;
+        }
+    }
 }
 
 // ------------------------------------------------------------ launchers
@@ -1680,6 +1724,9 @@ int mq_chunk_end(const mq_state *st, int iters, void *stream) {
 
 int mq_avg_materialize(const mq_market *mk, const mq_state *st, void *stream) {
     if (!mk || !st) return set_error(cudaErrorInvalidValue, "mq_avg_materialize: null argument");
+    if (st->ws_hdr)  // the screened rows' x and flags, from their slots
+        ws_flush_kernel<<<grid_for(mk->n, 256, sm_count() * 16), 256, 0, (cudaStream_t)stream>>>(
+            mk->n, mk->row_ptr, *st);
     avg_materialize_kernel<<<grid_for(mk->nnz, 256, sm_count() * 16), 256, 0,
                              (cudaStream_t)stream>>>(mk->nnz, st->xsum, st->xbar, st->navg);
     return check_launch("mq_avg_materialize");

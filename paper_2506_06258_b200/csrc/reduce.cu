@@ -116,6 +116,123 @@ resid_rows_kernel(const mq_market mk, const double *__restrict__ x, double2 *__r
     }
 }
 
+// Both residual row passes of a check (kkt.py:29-87 for the last iterate
+// (x, p) and the average (xbar, pbar)) in one sweep: u, col and the x > 0
+// flags are read once, x only where flagged, xbar densely, and one 32-byte
+// slot per good holds (p, its column max, pbar, its column max), so an entry
+// costs one random sector for both.  Same row assignment, lane sums and
+// block partials as resid_rows_kernel: bitwise the two separate passes.
+template <int G>
+__global__ void __launch_bounds__(256)
+resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
+                  const uint8_t *__restrict__ xflag, const double *__restrict__ xbar,
+                  double4 *__restrict__ pc4, double *__restrict__ sa, double *__restrict__ sb) {
+    const double *__restrict__ U = mk.u_orig;
+    constexpr int RPW = 32 / G;
+    const int lane = threadIdx.x & (G - 1);
+    const int gsub = (threadIdx.x & 31) / G;
+    const int64_t warp_id = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double ym[2] = {0.0, 0.0}, gm[2] = {0.0, 0.0}, xm[2] = {0.0, 0.0}, em[2] = {0.0, 0.0};
+    double obj[2] = {0.0, 0.0}, nbad[2] = {0.0, 0.0};
+    double *misc[2] = {sa + kMisc, sb + kMisc};
+    for (int64_t base = warp_id * RPW; base < mk.n; base += nwarps * RPW) {
+        const int64_t i = base + gsub;
+        const bool has = i < mk.n;
+        int64_t a = 0, b = 0;
+        if (has) {
+            a = mk.row_ptr[i];
+            b = mk.row_ptr[i + 1];
+        }
+        double tp = 0.0, tq = 0.0;
+        for (int64_t t = a + lane; t < b; t += G) {
+            const double ut = U[t];
+            if (xflag[t]) tp += ut * x[t];  // zero entries add +0.0 exactly
+            tq += ut * xbar[t];
+        }
+        const double ti[2] = {group_sum<G>(tp), group_sum<G>(tq)};
+        bool ok[2];
+        double y[2] = {0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            ok[k] = has && ti[k] > 0.0;
+            if (has && !ok[k] && lane == 0) {
+                nbad[k] += 1.0;
+                atomicMin((unsigned long long *)(misc[k] + 4),
+                          (unsigned long long)(mk.row_begin + i));
+            }
+            if (ok[k]) {
+                y[k] = mk.w[i] / ti[k];
+                if (lane == 0) {
+                    obj[k] += mk.w[i] * log(ti[k]);
+                    ym[k] = fmax(ym[k], y[k]);
+                }
+            }
+        }
+        if (!ok[0] && !ok[1]) continue;
+        for (int64_t t = a + lane; t < b; t += G) {
+            const int32_t j = mk.col[t];
+            const double ut = U[t];
+            const double2 q01 = __ldcg(reinterpret_cast<const double2 *>(pc4 + j));
+            const double2 q23 = __ldcg(reinterpret_cast<const double2 *>(pc4 + j) + 1);
+            const double4 q = make_double4(q01.x, q01.y, q23.x, q23.y);
+            if (ok[0]) {
+                const double uy = ut * y[0];
+                if (uy > q.y) atomic_max_nonneg(reinterpret_cast<double *>(pc4 + j) + 1, uy);
+                const double es = fmax(q.x - uy, 0.0);
+                const double xv = xflag[t] ? x[t] : 0.0;
+                gm[0] = fmax(gm[0], xv * es);
+                xm[0] = fmax(xm[0], fabs(xv));
+                em[0] = fmax(em[0], es);
+            }
+            if (ok[1]) {
+                const double uy = ut * y[1];
+                if (uy > q.w) atomic_max_nonneg(reinterpret_cast<double *>(pc4 + j) + 3, uy);
+                const double es = fmax(q.z - uy, 0.0);
+                const double xv = xbar[t];
+                gm[1] = fmax(gm[1], xv * es);
+                xm[1] = fmax(xm[1], fabs(xv));
+                em[1] = fmax(em[1], es);
+            }
+        }
+    }
+    __shared__ double sm[32];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const double a0 = group_max<32>(ym[k]), a1 = group_max<32>(gm[k]);
+        const double a2 = group_max<32>(xm[k]), a3 = group_max<32>(em[k]);
+        if ((threadIdx.x & 31) == 0) {
+            atomic_max_nonneg(misc[k] + 0, a0);
+            atomic_max_nonneg(misc[k] + 1, a1);
+            atomic_max_nonneg(misc[k] + 2, a2);
+            atomic_max_nonneg(misc[k] + 3, a3);
+        }
+        const double ob = block_sum(obj[k], sm);
+        const double nb = block_sum(nbad[k], sm);
+        double *sc = k ? sb : sa;
+        if (threadIdx.x == 0) {
+            sc[kSlotObj * MQ_MAX_BLOCKS + blockIdx.x] = ob;
+            sc[kSlotBad * MQ_MAX_BLOCKS + blockIdx.x] = nb;
+        }
+    }
+}
+
+__global__ void pc4_init_kernel(int64_t m, const double *__restrict__ p,
+                                const double *__restrict__ pbar, double4 *__restrict__ pc4) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x)
+        pc4[j] = make_double4(p[j], 0.0, pbar[j], 0.0);
+}
+__global__ void pc4_out_kernel(int64_t m, const double4 *__restrict__ pc4,
+                               double *__restrict__ cb0, double *__restrict__ cb1) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const double4 q = pc4[j];
+        cb0[j] = fmax(cb0[j], q.y);
+        cb1[j] = fmax(cb1[j], q.w);
+    }
+}
+
 __global__ void pc_init_kernel(int64_t m, const double *__restrict__ p, double2 *__restrict__ pc) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m;
          j += (int64_t)gridDim.x * blockDim.x)
@@ -282,6 +399,30 @@ int mq_resid_rows(const mq_market *mk, const double *x, const double *p, int use
     sum_slots_kernel<<<1, 64, 0, s>>>(scratch, grid, 2, scratch + kMisc + 16);
     resid_rows_finish<<<1, 1, 0, s>>>(scratch, scratch + kMisc + 16, row_out);
     return check_launch("mq_resid_rows");
+}
+
+int mq_resid_rows_pair(const mq_market *mk, const mq_state *st, double *colbest_last,
+                       double *colbest_avg, double *work, double *row_out_last,
+                       double *row_out_avg, double *scratch_last, double *scratch_avg,
+                       void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!mk || !st || !work) return set_error(cudaErrorInvalidValue, "mq_resid_rows_pair: null");
+    const int grid = grid_for(mk->n, 8, MQ_MAX_BLOCKS);
+    for (double *sc : {scratch_last, scratch_avg}) {
+        cudaMemsetAsync(sc + kMisc, 0, 4 * sizeof(double), s);
+        cudaMemsetAsync(sc + kMisc + 4, 0xff, sizeof(double), s);
+    }
+    double4 *pc4 = reinterpret_cast<double4 *>(work);
+    const int gm = grid_for(mk->m, 256, MQ_MAX_BLOCKS);
+    pc4_init_kernel<<<gm, 256, 0, s>>>(mk->m, st->p, st->pbar, pc4);
+    resid_pair_kernel<8><<<grid, 256, 0, s>>>(*mk, st->x, st->xflag, st->xbar, pc4, scratch_last,
+                                              scratch_avg);
+    pc4_out_kernel<<<gm, 256, 0, s>>>(mk->m, pc4, colbest_last, colbest_avg);
+    sum_slots_kernel<<<1, 64, 0, s>>>(scratch_last, grid, 2, scratch_last + kMisc + 16);
+    resid_rows_finish<<<1, 1, 0, s>>>(scratch_last, scratch_last + kMisc + 16, row_out_last);
+    sum_slots_kernel<<<1, 64, 0, s>>>(scratch_avg, grid, 2, scratch_avg + kMisc + 16);
+    resid_rows_finish<<<1, 1, 0, s>>>(scratch_avg, scratch_avg + kMisc + 16, row_out_avg);
+    return check_launch("mq_resid_rows_pair");
 }
 
 int mq_resid_cols(int64_t m, const double *cs, const double *p, const double *colbest,

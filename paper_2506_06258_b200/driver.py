@@ -107,6 +107,30 @@ class _Fingerprint:
         return self.value
 
 
+class _DeviceFingerprint(_Fingerprint):
+    """instance_fingerprint of a device-resident instance (fileio.load_device),
+    streamed back on a side thread and its own CUDA stream."""
+
+    def __init__(self, dm, budgets):
+        import threading
+
+        import torch
+
+        self.value = ""
+        dev = dm.device
+        stream = torch.cuda.Stream(device=dev)
+        stream.wait_stream(torch.cuda.current_stream(dev))
+
+        def run():
+            from .fileio import device_fingerprint
+
+            with torch.cuda.device(dev), torch.cuda.stream(stream):
+                self.value = device_fingerprint(dm, budgets)
+
+        self.thread = threading.Thread(target=run, daemon=True)
+        self.thread.start()
+
+
 def device_violations(dm):
     """validate() (instance.py:87-115) evaluated on the device copy."""
     import torch
@@ -286,6 +310,17 @@ def run_solve(inst, cfg, algo, warm_start=None):
         if cfg.group is None:
             raise ValueError("a FisherShard is solved with SolveConfig.group set")
         return _run_solve_sharded(inst, cfg, algo, warm_start, world)
+    from .fileio import DeviceFisherInstance
+
+    if isinstance(inst, DeviceFisherInstance):  # streamed into device CSR (fileio)
+        dm = inst.dm
+        violations = device_violations(dm)
+        if violations:
+            raise ValidationError("; ".join(violations))
+        fp = _DeviceFingerprint(dm, inst.budgets)
+        session = DeviceSession(None, cfg, dm=dm, algo=algo)
+        return solve_on_device(session, cfg, warm_start=warm_start,
+                               w_sum=float(np.sum(inst.budgets)), fingerprint=fp, algo=algo)
     if not isinstance(inst, FisherInstance):
         raise TypeError(f"unsupported instance type {type(inst)!r}")
     from .device import DeviceMarket

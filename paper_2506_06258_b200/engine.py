@@ -169,6 +169,14 @@ class NativeOps:
                                        nat.ptr(out), nat.ptr(scratch), _cur_stream()),
                 "mq_resid_rows")
 
+    def resid_pair(self, cb_last, cb_avg, out_last, out_avg):
+        e = self.eng
+        self._c(self.lib.mq_resid_rows_pair(self.dm.struct, e.state, nat.ptr(cb_last),
+                                            nat.ptr(cb_avg), nat.ptr(e.resid_work),
+                                            nat.ptr(out_last), nat.ptr(out_avg),
+                                            nat.ptr(e.scratch), nat.ptr(e.scratch2),
+                                            _cur_stream()), "mq_resid_rows_pair")
+
     def resid_cols(self, cs, p, colbest, out, scratch):
         self._c(self.lib.mq_resid_cols(self.dm.m, nat.ptr(cs), nat.ptr(p), nat.ptr(colbest),
                                        nat.ptr(out), nat.ptr(scratch), _cur_stream()),
@@ -286,7 +294,8 @@ class PdhcgEngine:
         self.csbar = torch.zeros(m, **f64)
         self.cs0 = torch.zeros(m, **f64)
         self.colbest = torch.zeros(2, m, **f64)
-        self.resid_work = torch.zeros(2 * max(1, m), **f64)  # (p, column max) interleaved
+        # (p, column max[, pbar, column max]) interleaved per good
+        self.resid_work = torch.zeros(4 * max(1, m), **f64)
         self.steps = torch.zeros(2, **f64)
         self.navg_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         # [0] rows whose solve did not settle, [1] entries beyond the
@@ -549,6 +558,9 @@ class PdhcgEngine:
         self.colbest[k].zero_()
         self.ops.resid_rows(x, p, use_norm, self.colbest[k], t_out, self.out[16 * k: 16 * k + 8],
                             self.scratch if k == 0 else self.scratch2)
+        self._reduce_rows(k)
+
+    def _reduce_rows(self, k):
         if self.distributed:
             o = self.out[16 * k: 16 * k + 8]
             self._allreduce(self.colbest[k], "max")
@@ -580,10 +592,18 @@ class PdhcgEngine:
                          float(max(r_primal, r_dual, r_gap)))
 
     def residuals_pair(self):
-        """(last, avg) residuals on the ORIGINAL instance with one sync."""
-        self._rows(self.x, self.p, 0, 0)
+        """(last, avg) residuals on the ORIGINAL instance with one sync; with
+        the sparse iterate both row passes run as one sweep (mq_resid_rows_pair)."""
+        if self.sparse and isinstance(self.ops, NativeOps):
+            self.colbest.zero_()
+            self.ops.resid_pair(self.colbest[0], self.colbest[1], self.out[0:8],
+                                self.out[16:24])
+            self._reduce_rows(0)
+            self._reduce_rows(1)
+        else:
+            self._rows(self.x, self.p, 0, 0)
+            self._rows(self.xbar, self.pbar, 0, 1)
         self._cols(self.cs, self.p, 0)
-        self._rows(self.xbar, self.pbar, 0, 1)
         self._cols(self.csbar, self.pbar, 1)
         v = self.out.cpu().numpy()
         return self._assemble(v[0:16]), self._assemble(v[16:32])

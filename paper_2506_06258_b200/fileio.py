@@ -216,3 +216,150 @@ def load(prefix, fmt="mtx"):
     if os.path.exists(e_path):
         return ExchangeInstance(utilities, reader(e_path))
     raise ParseError(f"neither {w_path} nor {e_path} exists", path=prefix)
+
+
+# ------------------------------------------------------- streamed device ingest
+class DeviceFisherInstance:
+    """A Fisher instance read from its files straight into device CSR
+    (load_device): the DeviceMarket and the host budgets.  run_solve accepts
+    it like a FisherInstance; no host copy of the utility matrix exists."""
+
+    def __init__(self, dm, budgets, source):
+        self.dm = dm
+        self.budgets = budgets
+        self.source = source
+
+    @property
+    def n_buyers(self):
+        return self.dm.n
+
+    @property
+    def n_goods(self):
+        return self.dm.m
+
+
+def _size_line(path, fmt):
+    """(n_rows, n_cols, nnz, lines before the entries) from the header."""
+    with open(path) as fh:
+        if fmt == "csv":
+            parts = fh.readline().strip().split(",")
+            return int(parts[0]), int(parts[1]), int(parts[2]), 1
+        fh.readline()
+        skip = 1
+        for line in fh:
+            skip += 1
+            if not line.lstrip().startswith("%"):
+                parts = line.split()
+                return int(parts[0]), int(parts[1]), int(parts[2]), skip
+    raise ValueError("no size line")
+
+
+def load_device(prefix, fmt="mtx", device=None, chunk_entries=1 << 24):
+    """Fisher instance files (`P.u.<fmt>` + `P.w.txt`) parsed in chunks and
+    streamed into device CSR (the reference reader's semantics,
+    fileio.py:36-139 + SparseMatrix.from_triplets: zeros dropped, entries
+    sorted by (row, column), duplicates rejected).  The host parses chunk
+    k+1 (pandas' C tokenizer) while chunk k's H2D copy runs; validation,
+    the sort and the row offsets run on the device.  A file the fast path
+    cannot take (malformed lines, out-of-range or negative entries, a wrong
+    count) is re-read by the host reader, which raises the reference's
+    ParseError with its line number."""
+    import pandas as pd
+    import torch
+
+    from .device import DeviceMarket
+
+    u_path, w_path = f"{prefix}.u.{fmt}", f"{prefix}.w.txt"
+    if fmt not in FORMATS:
+        raise ValueError(f"unknown format {fmt!r}; expected one of {FORMATS}")
+    if not os.path.exists(u_path):
+        raise ParseError(f"no utility matrix at {u_path}", path=u_path)
+    if not os.path.exists(w_path):
+        raise ParseError(f"{w_path} does not exist (device ingest reads Fisher instances)",
+                         path=prefix)
+    dev = torch.device(device if device is not None else "cuda")
+
+    def host_reader():  # the exact errors
+        _, reader = _matrix_io(fmt)
+        reader(u_path)
+        raise ParseError("unreadable entry block", path=u_path)
+
+    try:
+        n, m, nnz, skip = _size_line(u_path, fmt)
+    except (ValueError, IndexError):
+        host_reader()
+    budgets = read_budgets(w_path)
+    if budgets.shape != (n,):
+        raise StructureError(f"{w_path} holds {len(budgets)} budgets but U has {n} rows")
+    base = 1 if fmt == "mtx" else 0
+    rows = torch.empty(nnz, dtype=torch.int64, device=dev)
+    cols = torch.empty(nnz, dtype=torch.int64, device=dev)
+    vals = torch.empty(nnz, dtype=torch.float64, device=dev)
+    stage = [None, None]
+    ev = [None, None]
+    off = 0
+    try:
+        reader = pd.read_csv(u_path, sep=" " if fmt == "mtx" else ",", header=None,
+                             skiprows=skip, comment="%" if fmt == "mtx" else None,
+                             names=[0, 1, 2], dtype={0: np.int64, 1: np.int64, 2: np.float64},
+                             engine="c", chunksize=chunk_entries, skip_blank_lines=True,
+                             float_precision="round_trip")  # correctly rounded, as float()
+        for k, df in enumerate(reader):
+            c = len(df)
+            if off + c > nnz:
+                host_reader()
+            b = k & 1
+            if ev[b] is not None:
+                ev[b].synchronize()  # the staging buffer's previous copy is done
+            stage[b] = [torch.from_numpy(df[j].to_numpy()).pin_memory() for j in (0, 1, 2)]
+            rows[off:off + c].copy_(stage[b][0], non_blocking=True)
+            cols[off:off + c].copy_(stage[b][1], non_blocking=True)
+            vals[off:off + c].copy_(stage[b][2], non_blocking=True)
+            ev[b] = torch.cuda.Event()
+            ev[b].record()
+            off += c
+    except (ValueError, pd.errors.ParserError, OverflowError):
+        host_reader()
+    if off != nnz:
+        host_reader()
+    rows -= base
+    cols -= base
+    bad = ((rows < 0) | (rows >= n) | (cols < 0) | (cols >= m) | (vals < 0)).any()
+    if bool(bad.item()):
+        host_reader()
+    keep = vals != 0.0
+    if not bool(keep.all().item()):
+        rows, cols, vals = rows[keep], cols[keep], vals[keep]
+    del keep
+    key = rows * m + cols
+    del rows
+    if bool((key[1:] < key[:-1]).any().item()):
+        key, order = torch.sort(key, stable=True)
+        cols, vals = cols[order], vals[order]
+        del order
+    if key.numel() > 1 and bool((key[1:] == key[:-1]).any().item()):
+        raise StructureError("duplicate entry in triplets")
+    counts = torch.bincount(torch.div(key, m, rounding_mode="floor"), minlength=n)
+    del key
+    row_ptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(counts, 0, out=row_ptr[1:])
+    dm = DeviceMarket(row_ptr, cols.to(torch.int32), vals, budgets, m, device=dev)
+    return DeviceFisherInstance(dm, budgets, prefix)
+
+
+def device_fingerprint(dm, budgets, chunk=1 << 23):
+    """instance_fingerprint (report.py:19-36) of a device-resident Fisher
+    instance, its arrays streamed back chunk by chunk: byte-identical to the
+    fingerprint of the same instance held on the host."""
+    import hashlib
+
+    import torch
+
+    h = hashlib.sha256()
+    h.update(np.int64([dm.n, dm.m]).tobytes())
+    for t, dt in ((dm.row_ptr, torch.int64), (dm.col, torch.int64), (dm.u_orig, torch.float64)):
+        for o in range(0, t.numel(), chunk):
+            h.update(t[o:o + chunk].to(dt).cpu().numpy().tobytes())
+    h.update(b"fisher")
+    h.update(np.ascontiguousarray(budgets, dtype=np.float64))
+    return h.hexdigest()

@@ -13,6 +13,7 @@
   reference's fp64 ascending-row sums over 200 iterations.
 """
 
+import gc
 import os
 
 import numpy as np
@@ -29,6 +30,19 @@ def _gpu():
 
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
+
+
+@pytest.fixture(autouse=True)
+def _release_device_memory():
+    """Config-4 markets take tens of GB: engines hold their captured graphs
+    in reference cycles, so collect them before the next test allocates."""
+    import gc
+
+    import torch
+
+    yield
+    gc.collect()
+    torch.cuda.empty_cache()
 
 
 def rel(a, b):
@@ -142,7 +156,8 @@ def test_c4_fixed_point_column_sums_track_fp64():
         eng.colsum(eng.x, ref)  # fp64, ascending rows
         torch.cuda.synchronize()
         res[mode] = (eng.p.cpu().numpy(), eng.cs.cpu().numpy(), ref.cpu().numpy())
-        del eng
+        del eng, ref
+        gc.collect()
         torch.cuda.empty_cache()
     p_fix, cs_fix, cs_ref = res[False]
     p_f64 = res[True][0]
@@ -151,3 +166,40 @@ def test_c4_fixed_point_column_sums_track_fp64():
     print(f"C4 fixed-point vs fp64: max |cs diff| {dcs:.2e}, price rel {dp:.2e}")
     assert dcs <= 1e-9
     assert dp <= 1e-9
+
+
+def test_c3_bitwise_run_to_run_determinism():
+    """SURVEY §5 / SPEC acceptance 9: two runs of the same solve segment on
+    config 3 (power-law rows: screened rows, the full-solve list, medium and
+    long rows, atomics everywhere) give bitwise identical iterates."""
+    import hashlib
+
+    import torch
+
+    from paper_2506_06258_b200.device import DeviceMarket
+    from paper_2506_06258_b200.engine import PdhcgEngine
+    from paper_2506_06258_b200.generate import generate_config
+
+    d = generate_config("c3", seed=0)
+    dm = DeviceMarket(d["row_ptr"], d["col"], d["u"], d["w"], d["m"])
+    del d
+    digests = []
+    for _ in range(2):
+        eng = PdhcgEngine(dm)
+        eng.initial_state()
+        eng.set_steps(0.02, 0.02)
+        passes = []
+        for _ in range(4):
+            passes += eng.run_chunk(40)
+        eng.restart()
+        passes += eng.run_chunk(40)
+        torch.cuda.synchronize()
+        h = hashlib.sha256()
+        for t in (eng.x, eng.p, eng.xbar, eng.pbar, eng.srow, eng.cs):
+            h.update(t.cpu().numpy().tobytes())
+        h.update(np.asarray(passes, dtype=np.int64).tobytes())
+        digests.append(h.hexdigest())
+        del eng
+        gc.collect()
+        torch.cuda.empty_cache()
+    assert digests[0] == digests[1]

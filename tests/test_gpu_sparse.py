@@ -92,3 +92,32 @@ def test_restart_resets_the_running_sum():
     assert np.all(eng.xflag[:eng.dm.nnz].cpu().numpy() == 1)
     eng.run_chunk(40)
     assert np.allclose(eng.xbar.cpu().numpy(), eng.xsum.cpu().numpy() / 40, rtol=1e-15)
+
+
+def test_fused_residual_pair_is_bitwise_the_two_passes():
+    """mq_resid_rows_pair (one sweep for the last and the averaged iterate)
+    against the two separate mq_resid_rows passes, mid-solve on a generated
+    market with medium rows: identical residuals and column maxima."""
+    import torch
+
+    from paper_2506_06258_b200.device import DeviceMarket
+    from paper_2506_06258_b200.engine import PdhcgEngine
+    from paper_2506_06258_b200.generate import generate_rows
+
+    d = generate_rows(30_000, 3_000, seed=6, powerlaw=2.0, mean_degree=40.0)
+    eng = PdhcgEngine(DeviceMarket(d["row_ptr"], d["col"], d["u"], d["w"], d["m"]))
+    eng.initial_state()
+    eng.set_steps(0.05, 0.05)
+    for _ in range(3):
+        eng.run_chunk(40)
+    fused = eng.residuals_pair()
+    out_f, cb_f = eng.out.clone(), eng.colbest.clone()
+    eng._rows(eng.x, eng.p, 0, 0)
+    eng._cols(eng.cs, eng.p, 0)
+    eng._rows(eng.xbar, eng.pbar, 0, 1)
+    eng._cols(eng.csbar, eng.pbar, 1)
+    torch.cuda.synchronize()
+    v = eng.out.cpu().numpy()
+    sep = (eng._assemble(v[0:16]), eng._assemble(v[16:32]))
+    assert fused == sep
+    assert torch.equal(out_f, eng.out) and torch.equal(cb_f, eng.colbest)

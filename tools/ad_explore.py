@@ -31,6 +31,10 @@ CONFIGS = {
     "fixed_1000": dict(restart="fixed", restart_k=1000),
     "check_10": dict(check_every=10),
     "max_iters_20k": dict(max_iters=20_000),
+    "max_iters_1m": dict(max_iters=1_000_000),
+    "theory_1m": dict(step_mode="theory", max_iters=1_000_000),
+    "check_10_1m": dict(check_every=10, max_iters=1_000_000),
+    "beta_art_05": dict(restart_params=mq.RestartParams(0.2, 0.8, 0.5)),
 }
 for seed in [int(s) for s in a.seeds.split(",")]:
     ex = mq.generate_exchange(mq.GeneratorConfig(n=1000, m=400, sparsity_u=0.2, sparsity_e=0.5,
