@@ -253,6 +253,8 @@ def traffic_from_profile(name, config):
 
 # ------------------------------------------------------------------ CPU side
 
+REF_BUDGET_S = 300.0  # the reference arm's timed steps (whole-market iterations)
+
 def host_copy(shard):
     """Host arrays of this rank's shard (the e2e input and the CPU legs)."""
     from paper_2506_06258_b200.engine import to_host
@@ -512,18 +514,26 @@ def reference_arm(a, rank, world):
     nnz = int(host["row_ptr"][-1])
     run, setup_s = cpu_chunk_run(host, threads)
     del host
-    for _ in range(a.warmup):
+    # every step is one whole-market iteration; the run stays within
+    # REF_BUDGET_S: at most 2 warm-up iterations (a C kernel needs no JIT
+    # warm-up) and K timed ones unless K of them would exceed the budget
+    warm = max(1, min(a.warmup, 2))
+    tw = time.perf_counter()
+    for _ in range(warm):
         run.step(1)
+    t_it = (time.perf_counter() - tw) / warm
+    steps = int(max(3, min(a.steps, REF_BUDGET_S // max(t_it, 1e-9))))
     times, passes = [], 0
-    for _ in range(a.steps):
+    for _ in range(steps):
         t1 = time.perf_counter()
         passes += int(run.step(1).sum())
         times.append(time.perf_counter() - t1)
     total = sum(times)
-    rate = a.steps / total
+    rate = steps / total
     out = {
         "metric": METRIC, "value": round(rate, 6), "unit": "iter/s", "n_gpus": world,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(1e3 * total / a.steps, 3),
+        "steps": steps, "warmup": warm, "ms_per_step": round(1e3 * total / steps, 3),
+        "steps_requested": a.steps, "warmup_requested": a.warmup,
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": f"BASELINE config {a.config[1]}: {CONFIG_TEXT[a.config]}",
@@ -532,14 +542,14 @@ def reference_arm(a, rank, world):
                    "tau": run.tau, "sigma": run.sigma},
         "cpu_baseline": {"value": round(rate, 6), "unit": "iter/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"the whole market every step: iterations {a.warmup + 1}.."
-                                   f"{a.warmup + a.steps} from the initial state of the C "
+                         "sample": f"the whole market every step: iterations {warm + 1}.."
+                                   f"{warm + steps} from the initial state of the C "
                                    "oracle (restated kernels.pdhcg_chunk, bit-identical to the "
                                    "reference's numba kernel), tau/sigma of the solver's first "
                                    "restart window"},
         "e2e": {"value": round(rate, 6), "unit": "iter/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "passes_per_row_per_iteration": round(passes / a.steps / n, 3),
+        "passes_per_row_per_iteration": round(passes / steps / n, 3),
         "generate_seconds": round(gen_s, 2), "setup_seconds": round(setup_s, 2),
     }
     print(json.dumps(out), flush=True)

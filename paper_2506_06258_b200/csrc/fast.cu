@@ -1570,9 +1570,11 @@ __global__ void chunk_end_kernel(int64_t *navg, int iters) { *navg += iters; }
 __global__ void avg_materialize_kernel(int64_t nnz, const double *__restrict__ xsum,
                                        double *__restrict__ xbar, const int64_t *__restrict__ navg) {
     const double count = (double)*navg;
+    if (count <= 0.0) return;
+    const double inv = 1.0 / count;  // one division, not one per entry
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
          e += (int64_t)gridDim.x * blockDim.x)
-        xbar[e] = count > 0.0 ? xsum[e] / count : xbar[e];
+        xbar[e] = xsum[e] * inv;
 }
 
 // End of a chunk: x and its flags of every row with a working set, from the
@@ -1587,8 +1589,12 @@ __global__ void ws_flush_kernel(int64_t n, const int64_t *__restrict__ row_ptr, 
             const int64_t at = ws_at(i, k);
             const int64_t g = e0 + st.ws_pos[at];
             const double x = st.ws_x[at];
-            st.x[g] = x;
-            st.xflag[g] = x > 0.0;
+            const bool nz = x > 0.0;
+            const uint8_t f = st.xflag[g];  // x > 0 as of the last write-back
+            if (nz || f) {  // a zero that stayed zero needs no write
+                st.x[g] = x;
+                if (nz != (f != 0)) st.xflag[g] = nz;
+            }
         }
     }
 }

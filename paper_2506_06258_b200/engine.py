@@ -18,6 +18,7 @@ scalars per check.
 
 import math
 import os
+import weakref
 
 import numpy as np
 import torch
@@ -130,7 +131,9 @@ class NativeOps:
     supports_graphs = True
 
     def __init__(self, dm, engine):
-        self.lib, self.dm, self.eng = dm.lib, dm, engine
+        # a weak reference: no engine <-> ops cycle, so a dropped engine frees
+        # its device memory at once (config 4 holds tens of GB)
+        self.lib, self.dm, self.eng = dm.lib, dm, weakref.proxy(engine)
 
     def _c(self, rc, what):
         return nat.check(rc, what)
@@ -261,7 +264,9 @@ class PdhcgEngine:
         self.blk_done = torch.zeros(8, dtype=torch.int32, device=dev)
         # working sets of the screened row solve: -3 marks the
         # rows the medium / long kernels solve, -1 "no working set yet"
-        self.working_set = bool(working_set and self.sparse and hasattr(dm, "lib"))
+        # (the fp64 validation mode sums x itself mid-chunk: no slot-resident x)
+        self.working_set = bool(working_set and self.sparse and hasattr(dm, "lib")
+                                and not colsum_fp64)
         if self.working_set:
             K = nat.WS_SLOTS
             lens = dm.row_ptr[1:] - dm.row_ptr[:-1]

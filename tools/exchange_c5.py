@@ -2,7 +2,7 @@
 U and E each Bernoulli(0.01)), generated on device, solved through the
 public solve_exchange API (warm-started PDHCG inner solves on the B200).
 
-    python tools/exchange_c5.py [--n 100000] [--q 0.01] [--inner-max-iters 20000]
+    python tools/exchange_c5.py [--n 100000] [--q 0.01] [--inner-max-iters 100000]
 """
 import argparse
 import json
@@ -21,7 +21,7 @@ from paper_2506_06258_b200.generate import generate_rows  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=100_000)
 ap.add_argument("--q", type=float, default=0.01)
-ap.add_argument("--inner-max-iters", type=int, default=20000)
+ap.add_argument("--inner-max-iters", type=int, default=100_000)  # the reference default
 ap.add_argument("--max-outer", type=int, default=40)
 ap.add_argument("--outer-tol", type=float, default=1e-6)
 a = ap.parse_args()
