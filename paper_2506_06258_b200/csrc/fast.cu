@@ -197,6 +197,7 @@ __device__ __forceinline__ void aligned_span(const void *base, int64_t first, in
 // cs_xmax (a larger x_e is counted as a fault; device.py fixed_point_scale).
 __device__ __forceinline__ void fixed_colsum_add(const mq_market &mk, const mq_state &st, int j,
                                                  double xe) {
+    MQ_CHECK(j >= 0 && j < mk.m);
     if (xe < mk.cs_xmax) {
         asm volatile("red.global.add.u64 [%0], %1;" ::"l"(reinterpret_cast<unsigned long long *>(
                          st.bucket) + j),
@@ -210,6 +211,7 @@ __device__ __forceinline__ void fixed_colsum_add(const mq_market &mk, const mq_s
 // the dense array stays exact), the running sum and the column sum
 __device__ __forceinline__ void put_x(const mq_market &mk, const mq_state &st, int64_t e, int j,
                                       double xn, bool write_x) {
+    MQ_CHECK(e >= 0 && e < mk.nnz);
     const bool nz = xn > 0.0;
     st_flag(st.xflag + e, nz);
     if (nz || write_x) st.x[e] = xn;
@@ -423,6 +425,7 @@ __device__ __forceinline__ double row_root_warm(const double (&c)[PER], const do
 
 // slot k of row i: a warp's 32 consecutive rows read slot k as one run
 __device__ __forceinline__ int64_t ws_at(int64_t i, int k) {
+    MQ_CHECK(i >= 0 && k >= 0 && k < MQ_WS_SLOTS);
     return (((i >> 5) * MQ_WS_SLOTS + k) << 5) + (i & 31);
 }
 
@@ -437,7 +440,10 @@ __device__ __forceinline__ void ws_push(const mq_state &st, bool push, int64_t r
     int base = 0;
     if (wl == leader) base = atomicAdd(st.blk_done + 3, __popc(b));
     base = __shfl_sync(MQ_FULL, base, leader);
-    if (push) st.ws_list[base + __popc(b & ((1u << wl) - 1u))] = (int32_t)row;
+    if (push) {
+        MQ_CHECK(row >= 0 && base >= 0);
+        st.ws_list[base + __popc(b & ((1u << wl) - 1u))] = (int32_t)row;
+    }
 }
 
 // price-decrease bound of this iteration: C + dec, rounded up (the value the
@@ -489,6 +495,7 @@ __device__ __forceinline__ void ws_build(const mq_state &st, int64_t i, int lane
 #pragma unroll
         for (int e = 0; e < RP; ++e) {
             if ((hot >> e) & 1u) {
+                MQ_CHECK(rank[e] < before && lane + e * G < len);
                 const int64_t at = ws_at(i, rank[e]);
                 st.ws_u[at] = u[e];
                 st.ws_x[at] = xn[e];
@@ -882,8 +889,10 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
         const int64_t r = claimed;
         if (r >= mk.nlong) break;
         const int64_t i = mk.long_rows[r];
+        MQ_CHECK(i >= 0 && i < mk.n);
         const int64_t a = mk.row_ptr[i];
         const int len = (int)(mk.row_ptr[i + 1] - a);
+        MQ_CHECK(a >= 0 && a + len <= mk.nnz);
         const int ns = len < CAP ? len : CAP;
         const double tw = tau * mk.w[i];
         double *__restrict__ gx = st.x + a;
@@ -1037,8 +1046,10 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
         r = __shfl_sync(MQ_FULL, r, 0);
         if (r >= mk.nmed) break;  // warp-uniform
         const int64_t i = mk.med_rows[r];
+        MQ_CHECK(i >= 0 && i < mk.n);
         const int64_t e0 = mk.row_ptr[i];
         const int len = (int)(mk.row_ptr[i + 1] - e0);
+        MQ_CHECK(e0 >= 0 && e0 + len <= mk.nnz);
         const double tw = tau * mk.w[i];
         const double *__restrict__ su = mk.u + e0;
         const int32_t *__restrict__ cl = mk.col + e0;
@@ -1256,6 +1267,7 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
             e0 = d.rp[rl];
         }
         int h = has ? hd.x : -3;
+        MQ_CHECK(h >= -3 && h <= K);
         if (force_full && h != -3) h = -1;
         uint32_t was = 0;  // slots whose x was nonzero
 #pragma unroll
@@ -1266,6 +1278,7 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
             if (k < h) {
                 u[k] = d.u[so + k * 32];
                 c[k] = d.x[so + k * 32];
+                MQ_CHECK(d.col[so + k * 32] >= 0 && d.col[so + k * 32] < mk.m);
                 pv[k] = __ldg(st.p + d.col[so + k * 32]);
                 if (c[k] > 0.0) was |= 1u << k;
             }
@@ -1357,6 +1370,7 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
                     const int64_t at = ws_at(i, k);
                     pos[k] = __ldcg(st.ws_pos + at);
                     jc[k] = __ldcg(st.ws_col + at);
+                    MQ_CHECK(e0 + pos[k] < mk.nnz && jc[k] >= 0 && jc[k] < mk.m);
                 }
             }
 #pragma unroll
@@ -1406,6 +1420,7 @@ ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict
         const int r = rb + gsub;
         const bool has = r < count;
         const int64_t i = has ? st.ws_list[r] : 0;
+        MQ_CHECK(count <= mk.n && i >= 0 && i < mk.n);
         int64_t a = 0;
         int len = 0;
         double w = 0.0, s0 = 0.0;
@@ -1416,6 +1431,7 @@ ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict
             w = __ldg(mk.w + i);
             s0 = st.srow[i];
             hold = __ldcg(st.ws_hdr + 4 * i);
+            MQ_CHECK(len <= RP * G && hold >= -2 && hold <= MQ_WS_SLOTS);
         }
         double c[RP], u[RP], pv[RP], xv[RP];
         int jc[RP];
@@ -1588,6 +1604,7 @@ __global__ void ws_flush_kernel(int64_t n, const int64_t *__restrict__ row_ptr, 
         for (int k = 0; k < h; ++k) {
             const int64_t at = ws_at(i, k);
             const int64_t g = e0 + st.ws_pos[at];
+            MQ_CHECK(g < row_ptr[i + 1]);
             const double x = st.ws_x[at];
             const bool nz = x > 0.0;
             const uint8_t f = st.xflag[g];  // x > 0 as of the last write-back

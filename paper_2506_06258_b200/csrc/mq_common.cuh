@@ -7,6 +7,16 @@
 #include "market_eq_b200.h"
 
 #define MQ_FULL 0xffffffffu
+
+// Bounds checks of the checked build (-DMQ_DEBUG_BOUNDS; compute-sanitizer is
+// not available on the GPU pool): a failed check prints its file and line and
+// traps, the launch fails and the caller's NativeError names the call.
+#ifdef MQ_DEBUG_BOUNDS
+#include <cassert>
+#define MQ_CHECK(c) assert(c)
+#else
+#define MQ_CHECK(c) ((void)0)
+#endif
 #define MQ_MAX_BLOCKS 1024          // fixed partial-sum width => deterministic sums
 #define MQ_SCRATCH_DOUBLES (8 * MQ_MAX_BLOCKS + 64)
 

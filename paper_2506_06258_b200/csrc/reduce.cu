@@ -172,6 +172,7 @@ resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
         if (!ok[0] && !ok[1]) continue;
         for (int64_t t = a + lane; t < b; t += G) {
             const int32_t j = mk.col[t];
+            MQ_CHECK(j >= 0 && j < mk.m);
             const double ut = U[t];
             const double2 q01 = __ldcg(reinterpret_cast<const double2 *>(pc4 + j));
             const double2 q23 = __ldcg(reinterpret_cast<const double2 *>(pc4 + j) + 1);

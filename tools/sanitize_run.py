@@ -50,7 +50,7 @@ def main():
     # lifted PDHG and the theory diagnostics
     mq.run_solve(inst, mq.SolveConfig(tol=1e-3, use_graphs=False, max_iters=400), "pdhg")
     rep = mq.run_solve(inst, mq.SolveConfig(tol=1e-4, max_iters=400), "pdhcg")
-    mq.smoothed_gap(inst, rep.allocation, rep.prices, 1.0)
+    mq.smoothed_gap(inst, (rep.allocation, rep.prices), (rep.allocation, rep.prices), 1.0)
     # exchange (E.p on the device)
     ex = mq.generate_exchange(mq.GeneratorConfig(n=60, m=30, sparsity_u=0.3, sparsity_e=0.5,
                                                  seed=2))
