@@ -69,6 +69,10 @@ timed_method(engine.PdhcgEngine, "__init__")
 timed_method(engine.PdhcgEngine, "final_payload")
 timed_method(engine.PdhcgEngine, "omega_norms")
 timed_method(engine.PdhcgEngine, "initial_state")
+timed_method(engine.PdhcgEngine, "residuals_pair")
+timed_method(engine.PdhcgEngine, "restart_moves")
+timed_method(engine.PdhcgEngine, "restart")
+timed_method(engine.PdhcgEngine, "run_chunk")
 timed_method(driver._Fingerprint, "get")
 timed(driver, "device_violations")
 torch.cuda.synchronize()
@@ -77,5 +81,14 @@ rep = mq.run_solve(inst, mq.SolveConfig(tol=1e-4, max_iters=a.iters), "pdhcg")
 wall = time.perf_counter() - T0[0]
 print(f"wall {wall:.2f} s for {rep.inner_iterations} iterations; device loop "
       f"{rep.device_stats.get('chunk_seconds', 0):.2f} s")
+from collections import defaultdict  # noqa: E402
+
+agg = defaultdict(lambda: [0, 0.0])
 for t, d, nm in sorted(LOG):
-    print(f"  start {t:7.3f}  took {d:7.3f}  {nm}")
+    agg[nm][0] += 1
+    agg[nm][1] += d
+    if agg[nm][0] <= 2:
+        print(f"  start {t:7.3f}  took {d:7.3f}  {nm}")
+print("totals:")
+for nm, (c, d) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    print(f"  {nm:40s} calls {c:6d}  total {d:8.3f} s  mean {1e3 * d / c:8.3f} ms")
