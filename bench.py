@@ -324,6 +324,10 @@ def main():
     # functional check of the N-rank path on a 1-GPU box: every rank on cuda:0,
     # gloo collectives (numbers meaningless; never used for measurements)
     shared = os.environ.get("MQ_BENCH_SHARED_GPU") == "1"
+    if a.impl == "reference":  # host cores only: no device, gloo for the barrier
+        if world > 1:
+            dist.init_process_group("gloo")
+        return reference_arm(a, rank, world)
     if shared:
         local = 0
     torch.cuda.set_device(local)
@@ -336,8 +340,6 @@ def main():
             os.environ.setdefault("NCCL_DEBUG", "INFO")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
-    if a.impl == "reference":
-        return reference_arm(a, rank, world)
 
     from paper_2506_06258_b200 import _build
 

@@ -170,30 +170,50 @@ resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
             }
         }
         if (!ok[0] && !ok[1]) continue;
-        for (int64_t t = a + lane; t < b; t += G) {
-            const int32_t j = mk.col[t];
-            MQ_CHECK(j >= 0 && j < mk.m);
-            const double ut = U[t];
-            const double2 q01 = __ldcg(reinterpret_cast<const double2 *>(pc4 + j));
-            const double2 q23 = __ldcg(reinterpret_cast<const double2 *>(pc4 + j) + 1);
-            const double4 q = make_double4(q01.x, q01.y, q23.x, q23.y);
-            if (ok[0]) {
-                const double uy = ut * y[0];
-                if (uy > q.y) atomic_max_nonneg(reinterpret_cast<double *>(pc4 + j) + 1, uy);
-                const double es = fmax(q.x - uy, 0.0);
-                const double xv = xflag[t] ? x[t] : 0.0;
-                gm[0] = fmax(gm[0], xv * es);
-                xm[0] = fmax(xm[0], fabs(xv));
-                em[0] = fmax(em[0], es);
+        // LB entries per lane per batch: every load of the batch (and its
+        // price-slot gather) is issued before the atomics that consume them
+        constexpr int LB = 4;
+        for (int64_t t0 = a + lane; t0 < b; t0 += LB * G) {
+            int32_t jv[LB];
+            double uv[LB], xv[LB], bv[LB];
+            double2 q01[LB], q23[LB];
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                const int64_t t = t0 + q * G;
+                const bool in = t < b;
+                jv[q] = in ? mk.col[t] : 0;
+                MQ_CHECK(jv[q] >= 0 && jv[q] < mk.m);
+                uv[q] = in ? U[t] : 0.0;
+                xv[q] = (in && xflag[t]) ? x[t] : 0.0;
+                bv[q] = in ? xbar[t] : 0.0;
             }
-            if (ok[1]) {
-                const double uy = ut * y[1];
-                if (uy > q.w) atomic_max_nonneg(reinterpret_cast<double *>(pc4 + j) + 3, uy);
-                const double es = fmax(q.z - uy, 0.0);
-                const double xv = xbar[t];
-                gm[1] = fmax(gm[1], xv * es);
-                xm[1] = fmax(xm[1], fabs(xv));
-                em[1] = fmax(em[1], es);
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                q01[q] = __ldcg(reinterpret_cast<const double2 *>(pc4 + jv[q]));
+                q23[q] = __ldcg(reinterpret_cast<const double2 *>(pc4 + jv[q]) + 1);
+            }
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                if (t0 + q * G >= b) continue;
+                const int32_t j = jv[q];
+                if (ok[0]) {
+                    const double uy = uv[q] * y[0];
+                    if (uy > q01[q].y)
+                        atomic_max_nonneg(reinterpret_cast<double *>(pc4 + j) + 1, uy);
+                    const double es = fmax(q01[q].x - uy, 0.0);
+                    gm[0] = fmax(gm[0], xv[q] * es);
+                    xm[0] = fmax(xm[0], fabs(xv[q]));
+                    em[0] = fmax(em[0], es);
+                }
+                if (ok[1]) {
+                    const double uy = uv[q] * y[1];
+                    if (uy > q23[q].y)
+                        atomic_max_nonneg(reinterpret_cast<double *>(pc4 + j) + 3, uy);
+                    const double es = fmax(q23[q].x - uy, 0.0);
+                    gm[1] = fmax(gm[1], bv[q] * es);
+                    xm[1] = fmax(xm[1], fabs(bv[q]));
+                    em[1] = fmax(em[1], es);
+                }
             }
         }
     }
