@@ -392,9 +392,13 @@ def resid_cases():
 
 # ----------------------------------------------------------------- exchange
 
-def exchange_case():
-    ex = me.generate_exchange(me.GeneratorConfig(n=40, m=30, sparsity_u=0.3,
-                                                 sparsity_e=0.5, seed=2))
+def exchange_case(name="exchange.npz", n=40, m=30, qu=0.3, qe=0.5, seed=2):
+    """The reference's fixed-point loop on a generated exchange instance.
+    exchange.npz: inner-failure (the reference's usual outcome);
+    exchange_converged.npz: an instance on which it converges
+    (tools/ad_search.py: 1 of 108 generated instances)."""
+    ex = me.generate_exchange(me.GeneratorConfig(n=n, m=m, sparsity_u=qu,
+                                                 sparsity_e=qe, seed=seed))
     t = time.time()
     tr = me.solve_exchange(ex, outer_tol=1e-6)
     t_ref = time.time() - t
@@ -407,14 +411,14 @@ def exchange_case():
     o = orc.solve_exchange(mkU, mkE, outer_tol=1e-6)
     assert o["status"] == tr.status and o["outer_iterations"] == tr.outer_iterations
     assert same(o["budget_gaps"], tr.budget_gaps) and same(o["final_prices"], tr.final_prices)
-    save("exchange.npz", n=U.n_rows, m=U.n_cols,
+    save(name, n=U.n_rows, m=U.n_cols,
          u_indptr=U.row_offsets, u_col=U.col_indices, u=U.values,
          e_indptr=E.row_offsets, e_col=E.col_indices, e=E.values,
          status=tr.status, outer=tr.outer_iterations, gaps=np.array(tr.budget_gaps),
          final_budgets=tr.final_budgets, final_prices=tr.final_prices,
          inner_iters=np.array([r.inner_iterations for r in tr.inner_reports]),
          ref_seconds=t_ref)
-    print(f"  exchange: {tr.status} outer={tr.outer_iterations} ref {t_ref:.1f}s")
+    print(f"  {name}: {tr.status} outer={tr.outer_iterations} ref {t_ref:.1f}s")
 
 
 # --------------------------------------------------------------- generators
@@ -519,7 +523,9 @@ def main():
              "pdhg": pdhg_cases, "theory": theory_case, "fileio": fileio_case,
              "bigsolve": big_solve_cases,
              "resid": resid_cases, "exchange": exchange_case,
-             "gen": lambda: gen_fingerprints(a.big), "c2": c2_lockstep, "c2solve": c2_solve}
+             "gen": lambda: gen_fingerprints(a.big), "c2": c2_lockstep, "c2solve": c2_solve,
+             "exchange_conv": lambda: exchange_case("exchange_converged.npz", 10, 6, 0.3, 1.0,
+                                                    2)}
     for k, fn in steps.items():
         if a.only and k not in a.only.split(","):
             continue

@@ -224,19 +224,29 @@ def test_analytic_single_buyer():
 
 # ------------------------------------------------------------ exchange
 
-def test_exchange_matches_reference():
+@pytest.mark.parametrize("name", ["exchange.npz", "exchange_converged.npz"])
+@pytest.mark.parametrize("solver", ["exact", "ksection"])
+def test_exchange_matches_reference(name, solver):
+    """solve_exchange (exchange.py:104-156) against the reference's own trace:
+    the usual inner-failure case and a case the reference's loop converges
+    on (outer count, every budget gap, final prices and budgets)."""
     import paper_2506_06258_b200 as mq
 
-    g = golden("exchange.npz")
+    g = golden(name)
     U = mq.SparseMatrix(int(g["n"]), int(g["m"]), g["u_indptr"], g["u_col"], g["u"])
     E = mq.SparseMatrix(int(g["n"]), int(g["m"]), g["e_indptr"], g["e_col"], g["e"])
-    tr = mq.solve_exchange(mq.ExchangeInstance(U, E), outer_tol=1e-6)
-    print(f"exchange: {tr.status} outer={tr.outer_iterations} (ref {str(g['status'])} "
+    tr = mq.solve_exchange(mq.ExchangeInstance(U, E), outer_tol=1e-6,
+                           inner_config=mq.SolveConfig(row_solver=solver))
+    print(f"{name} [{solver}]: {tr.status} outer={tr.outer_iterations} (ref {str(g['status'])} "
           f"{int(g['outer'])}), inner {[r.inner_iterations for r in tr.inner_reports]} "
           f"(ref {list(g['inner_iters'])})")
     assert tr.status == str(g["status"])
     assert tr.outer_iterations == int(g["outer"])
-    assert np.allclose(tr.budget_gaps, g["gaps"], rtol=1e-5)
+    assert [r.inner_iterations for r in tr.inner_reports] == list(g["inner_iters"])
+    assert np.allclose(tr.budget_gaps, g["gaps"], rtol=1e-5, atol=1e-12)
+    if tr.status == "converged":
+        assert rel_max(tr.final_prices, g["final_prices"]) <= 1e-6
+        assert np.allclose(tr.budgets_history[-1], g["final_budgets"], rtol=1e-6, atol=1e-12)
 
 
 # ------------------------------------------------------------ C2 lockstep

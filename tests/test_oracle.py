@@ -125,8 +125,9 @@ def test_oracle_residuals_bit_exact(oracle):
         assert oracle.eg_objective(mk, x) == obj
 
 
-def test_oracle_exchange_matches_reference(oracle):
-    g = golden("exchange.npz")
+@pytest.mark.parametrize("name", ["exchange.npz", "exchange_converged.npz"])
+def test_oracle_exchange_matches_reference(oracle, name):
+    g = golden(name)
     U = oracle.Market(int(g["n"]), int(g["m"]), g["u_indptr"], g["u_col"], g["u"],
                       np.ones(int(g["n"])))
     E = oracle.Market(int(g["n"]), int(g["m"]), g["e_indptr"], g["e_col"], g["e"],
