@@ -39,6 +39,7 @@ extern "C" {
 #define MQ_REG_ROW 128        /* tile rows longer than this (medium rows) are
                                  solved by the warp-per-row path          */
 #define MQ_WS_SLOTS 12        /* working-set slots per row (screened solve)  */
+#define MQ_WS_MAX_ROW 256     /* rows up to this length have working sets    */
 
 /* Read-only market description (device pointers, borrowed).  Arrays marked
  * [pad] must have 16 readable bytes past their last element (TMA bulk copies
@@ -63,6 +64,10 @@ typedef struct mq_market {
        kernel solves them, so no tile stage waits on one slow row             */
     const int32_t *med_rows;
     int64_t nmed;
+    /* the leading med_rows longer than MQ_WS_MAX_ROW: with working sets on,
+       the warp-per-row kernel solves only these (shorter rows have working
+       sets); without, or in a rebuild step, all nmed                       */
+    int64_t nmed_long;
     /* tile-blocked transpose schedule of the deterministic fp64 column sums
        (mq_colsum: residual checks, restarts): the tiles are grouped in blocks
        of tiles_per_block consecutive tiles; bperm lists, block by block and

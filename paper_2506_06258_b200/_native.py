@@ -20,6 +20,7 @@ TILE_ROWS = 256       # MQ_TILE_ROWS
 PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
 ABI_VERSION = 8
 WS_SLOTS = 12          # MQ_WS_SLOTS
+WS_MAX_ROW = 256       # MQ_WS_MAX_ROW
 
 _lock = threading.Lock()
 _lib = None
@@ -42,7 +43,7 @@ class MqMarket(ctypes.Structure):
     _fields_ = [("n", I64), ("m", I64), ("nnz", I64),
                 ("row_ptr", P), ("col", P), ("u", P), ("u_orig", P), ("w", P),
                 ("tiles", P), ("ntiles", I64), ("long_rows", P), ("nlong", I64),
-                ("med_rows", P), ("nmed", I64),
+                ("med_rows", P), ("nmed", I64), ("nmed_long", I64),
                 ("bperm", P), ("bptr", P), ("nblk", I64), ("tiles_per_block", I64),
                 ("prim_grid", ctypes.c_int32), ("row_begin", I64),
                 ("cs_scale", ctypes.c_double), ("cs_xmax", ctypes.c_double)]

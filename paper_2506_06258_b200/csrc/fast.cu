@@ -483,7 +483,8 @@ __device__ __forceinline__ void ws_build(const mq_state &st, int64_t i, int lane
             }
             pm = fmin(pm, pv[e]);
         }
-        const uint32_t bal = (__ballot_sync(MQ_FULL, hb) >> (gsub * G)) & ((1u << G) - 1u);
+        const uint32_t bal = G == 32 ? __ballot_sync(MQ_FULL, hb)
+                                     : (__ballot_sync(MQ_FULL, hb) >> (gsub * G)) & ((1u << (G & 31)) - 1u);
         rank[e] = before + __popc(bal & ((1u << lane) - 1u));
         before += __popc(bal);
     }
@@ -1035,7 +1036,8 @@ __global__ void __launch_bounds__(256, MQ_MED_MINB)
 #else
 __global__ void __launch_bounds__(256)
 #endif
-primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
+primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
+                  int64_t nrows) {
     constexpr int G = 32, LB = MQ_MED_LB;
     const double tau = st.steps[0];
     const int lane = threadIdx.x & 31;
@@ -1044,7 +1046,7 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
         int r = 0;
         if (lane == 0) r = atomicAdd(st.blk_done + 2, 1);
         r = __shfl_sync(MQ_FULL, r, 0);
-        if (r >= mk.nmed) break;  // warp-uniform
+        if (r >= nrows) break;  // warp-uniform
         const int64_t i = mk.med_rows[r];
         MQ_CHECK(i >= 0 && i < mk.n);
         const int64_t e0 = mk.row_ptr[i];
@@ -1405,16 +1407,16 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
 #endif
 __global__ void __launch_bounds__(256, MQ_WSF_MINB)
 ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
-    constexpr int G = 16, RP = MQ_REG_PER;
+    constexpr int G = 32, RP = MQ_WS_MAX_ROW / 32;  // a warp per row, rows <= 256 entries
     const double tau = st.steps[0];
     const double cnow = drift_now(st);
-    const int wl = threadIdx.x & 31, lane = wl & (G - 1), gsub = wl / G;
-    const uint32_t gmask = ((1u << G) - 1u) << (gsub * G);
+    const int wl = threadIdx.x & 31, lane = wl, gsub = 0;
+    const uint32_t gmask = MQ_FULL;
     const int count = *(volatile int32_t *)(st.blk_done + 3);
     int my_sweeps = 0, my_faults = 0;
     for (;;) {
         int rb = 0;
-        if (wl == 0) rb = atomicAdd(st.blk_done + 4, 2);
+        if (wl == 0) rb = atomicAdd(st.blk_done + 4, 1);
         rb = __shfl_sync(MQ_FULL, rb, 0);
         if (rb >= count) break;  // warp-uniform
         const int r = rb + gsub;
@@ -1459,7 +1461,7 @@ ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict
                     const double xk = __ldcg(st.ws_x + at);
 #pragma unroll
                     for (int e = 0; e < RP; ++e)
-                        if (e == (ps >> 4)) {
+                        if (e == ps / G) {
                             xv[e] = xk;
                             if (xk > 0.0) was |= 1u << e;
                         }
@@ -1689,9 +1691,12 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
         const int grid = grid_for(mk->nlong, 1, sm_count() * per_sm);
         lk<<<grid, MQ_LONG_THREADS, LS::kBytes, s>>>(*mk, *st, it, xprev);
     }
-    if (mk->nmed > 0) {
-        const int grid = grid_for(mk->nmed, 8, sm_count() * 8);
-        primal_med_kernel<<<grid, 256, 0, s>>>(*mk, *st, it, xprev);
+    // with working sets, medium rows up to MQ_WS_MAX_ROW entries are
+    // screened / fully solved above; the leading (longest) nmed_long stay here
+    const int64_t nmed = (st->ws_hdr && !st->ws_rebuild) ? mk->nmed_long : mk->nmed;
+    if (nmed > 0) {
+        const int grid = grid_for(nmed, 8, sm_count() * 8);
+        primal_med_kernel<<<grid, 256, 0, s>>>(*mk, *st, it, xprev, nmed);
     }
     return check_launch("mq_primal_step");
 }

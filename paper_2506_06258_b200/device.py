@@ -250,6 +250,10 @@ class DeviceMarket:
         s.nlong = int(self.long_rows.numel())
         s.med_rows = self.med_rows.data_ptr()
         s.nmed = int(self.med_rows.numel())
+        if s.nmed:  # med_rows is longest first
+            ml = (self.row_ptr[self.med_rows.to(torch.int64) + 1]
+                  - self.row_ptr[self.med_rows.to(torch.int64)])
+            s.nmed_long = int((ml > nat.WS_MAX_ROW).sum().item())
         s.bperm = self.bperm.data_ptr()
         s.bptr = self.bptr.data_ptr()
         s.nblk = int(self.nblk)

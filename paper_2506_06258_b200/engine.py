@@ -270,7 +270,7 @@ class PdhcgEngine:
         if self.working_set:
             K = nat.WS_SLOTS
             lens = dm.row_ptr[1:] - dm.row_ptr[:-1]
-            self.ws_init = torch.where(lens > int(dm.lib.mq_reg_row()), -3, -1).to(torch.int32)
+            self.ws_init = torch.where(lens > nat.WS_MAX_ROW, -3, -1).to(torch.int32)
             if dm.long_rows.numel():
                 self.ws_init[dm.long_rows.to(torch.int64)] = -3
             npad = -(-max(1, dm.n) // 32) * 32
