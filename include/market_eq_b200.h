@@ -152,6 +152,17 @@ typedef struct mq_state {
     double *drift;    /* [2] C = accumulated bound on the largest price
                          decrease (rounded up), this iteration's decrease
                          (bit pattern, order-free max)                      */
+    /* working sets of the long rows (> MQ_LONG_ROW entries, the CTA-per-row
+       kernel; pl_hdr == NULL: none), one pool of MQ_LONG_CAP entries per row
+       in mk.long_rows order: row r's working entries (ascending position) at
+       r * MQ_LONG_CAP + k, k < h; the header and certificate as ws_hdr's    */
+    int32_t *pl_hdr;  /* [4 nlong] h (-1 none, -2 more than MQ_LONG_CAP), theta,
+                         P, C (float bits, rounded down)                     */
+    double *pl_u;     /* [nlong MQ_LONG_CAP] normalized utility              */
+    double *pl_x;     /* its x (a long row's canonical x and flags are also
+                         written every iteration)                           */
+    int32_t *pl_col;  /* its good                                            */
+    int32_t *pl_pos;  /* its offset in the row                               */
     int32_t ws_rebuild; /* nonzero: this step runs the unscreened tile kernel
                            over every tile row and rebuilds all working sets
                            (after the host invalidated them; cheaper than
@@ -353,6 +364,8 @@ int mq_abi_version(void);
 int mq_fixed_colsum(void);
 /* working-set slots per row of this build (MQ_WS_SLOTS) */
 int mq_ws_slots(void);
+/* long-row working-set pool entries per row of this build (MQ_LONG_CAP) */
+int mq_long_cap(void);
 /* 1 if the build keeps the sparse iterate (xflag / xsum) */
 int mq_x_sparse(void);
 /* sparse iterate: xbar = xsum / navg (call after mq_chunk_end) */

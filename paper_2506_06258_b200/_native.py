@@ -21,6 +21,7 @@ PAD = 16              # padding elements after nnz arrays read by TMA bulk copie
 ABI_VERSION = 8
 WS_SLOTS = 12          # MQ_WS_SLOTS
 WS_MAX_ROW = 256       # MQ_WS_MAX_ROW
+LONG_CAP = 1536        # MQ_LONG_CAP (long-row working-set pool per row)
 
 _lock = threading.Lock()
 _lib = None
@@ -55,6 +56,7 @@ class MqState(ctypes.Structure):
                 ("pass_out", P), ("faults", P), ("bucket", P), ("srow", P),
                 ("xflag", P), ("xsum", P), ("ws_hdr", P), ("ws_kmax", P), ("ws_u", P),
                 ("ws_x", P), ("ws_col", P), ("ws_pos", P), ("ws_list", P), ("drift", P),
+                ("pl_hdr", P), ("pl_u", P), ("pl_x", P), ("pl_col", P), ("pl_pos", P),
                 ("ws_rebuild", ctypes.c_int32)]
 
 
@@ -99,6 +101,7 @@ _SIGS = {
     "mq_fixed_colsum": (CINT, []),
     "mq_x_sparse": (CINT, []),
     "mq_ws_slots": (CINT, []),
+    "mq_long_cap": (CINT, []),
     "mq_avg_materialize": (CINT, [PM, PS, P]),
     "mq_pdhg_step": (CINT, [PM, PL, CINT, P]),
     "mq_pdhg_colsum_only": (CINT, [PM, PL, CINT, P]),

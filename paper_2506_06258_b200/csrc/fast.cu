@@ -853,6 +853,33 @@ __device__ __forceinline__ void block_sum3(double &a, double &b, double &c, doub
     c = group_sum<32>(rc);
 }
 
+// Maxima of three values over the CTA (block_sum3's pattern).
+__device__ __forceinline__ void block_max3(double &a, double &b, double &c, double *sm /*[192]*/,
+                                           int &phase) {
+    a = group_max<32>(a);
+    b = group_max<32>(b);
+    c = group_max<32>(c);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+    double *buf = sm + 96 * (phase & 1);
+    ++phase;
+    if (lane == 0) {
+        buf[warp] = a;
+        buf[32 + warp] = b;
+        buf[64 + warp] = c;
+    }
+    __syncthreads();
+    double ra = -CUDART_INF, rb = -CUDART_INF, rc = -CUDART_INF;
+    if (lane < nw) {
+        ra = buf[lane];
+        rb = buf[32 + lane];
+        rc = buf[64 + lane];
+    }
+    a = group_max<32>(ra);
+    b = group_max<32>(rb);
+    c = group_max<32>(rc);
+}
+
 // One CTA per long row (rows claimed longest first from a global counter).
 // The row's first MQ_LONG_CAP entries stay in shared memory across the
 // sweeps (u, c = x - tau p[col], col, was-nonzero flag: 21 bytes per entry),
@@ -862,7 +889,8 @@ __device__ __forceinline__ void block_sum3(double &a, double &b, double &c, doub
 // so each thread re-reads only what it wrote.
 template <int T, int CAP>
 struct LongSmem {
-    static constexpr int kU = 0, kC = CAP * 8, kJ = 2 * CAP * 8, kF = kJ + CAP * 4;
+    static constexpr int kU = 0, kC = CAP * 8, kJ = 2 * CAP * 8, kP = kJ + CAP * 4;
+    static constexpr int kF = kP + CAP * 4;
     static constexpr int kBytes = kF + CAP;
 };
 
@@ -874,9 +902,12 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
     double *s_u = reinterpret_cast<double *>(lsm + L::kU);
     double *s_c = reinterpret_cast<double *>(lsm + L::kC);
     int32_t *s_j = reinterpret_cast<int32_t *>(lsm + L::kJ);
+    int32_t *s_p = reinterpret_cast<int32_t *>(lsm + L::kP);  // working-set positions
     uint8_t *s_f = lsm + L::kF;
     __shared__ double sm[192];
     __shared__ int64_t claimed;
+    __shared__ int wtot[T / 32 + 1];  // per-warp counts of a working-set rebuild chunk
+    const double cnow = st.pl_hdr ? drift_now(st) : 0.0;
     int phase = 0;
     const double tau = st.steps[0];
     const int tid = threadIdx.x;
@@ -895,8 +926,97 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
         const int len = (int)(mk.row_ptr[i + 1] - a);
         MQ_CHECK(a >= 0 && a + len <= mk.nnz);
         const int ns = len < CAP ? len : CAP;
-        const double tw = tau * mk.w[i];
+        const double wi = mk.w[i];
+        const double tw = tau * wi;
         double *__restrict__ gx = st.x + a;
+        // ---- screened solve over the row's working set (pool r): the same
+        // certificate as the short rows'
+        if (st.pl_hdr && !x_prev_out) {
+            const int4 hd = reinterpret_cast<const int4 *>(st.pl_hdr)[r];
+            const int h = hd.x;
+            MQ_CHECK(h >= -2 && h <= CAP);
+            if (h >= 0) {
+                const int64_t po = r * (int64_t)CAP;
+                double s0w = 0.0, Aw = 0.0, Bw = 0.0;
+                for (int k = tid; k < h; k += T) {
+                    const double ue = st.pl_u[po + k], xe = st.pl_x[po + k];
+                    const int j = st.pl_col[po + k];
+                    MQ_CHECK(j >= 0 && j < mk.m && st.pl_pos[po + k] < len);
+                    const double ce = xe - tau * __ldg(st.p + j);
+                    s_u[k] = ue;
+                    s_c[k] = ce;
+                    s_j[k] = j;
+                    s_p[k] = st.pl_pos[po + k];
+                    s_f[k] = xe > 0.0;
+                    s0w += ue * xe;
+                    Aw += ue * ce;
+                    Bw += ue * ue;
+                }
+                block_sum3(s0w, Aw, Bw, sm, phase);
+                double sw = active_root(Aw, Bw, tw);
+                int prev = h, nsw = 0;
+                bool ok = false;
+                auto wsweep = [&](double q, double &As, double &Bs, double &cnt) {
+                    As = Bs = cnt = 0.0;
+                    for (int k = tid; k < h; k += T) {
+                        const double ue = s_u[k], ce = s_c[k];
+                        if (fma(ce, q, tw * ue) > 0.0) {
+                            As += ue * ce;
+                            Bs += ue * ue;
+                            cnt += 1.0;
+                        }
+                    }
+                    block_sum3(As, Bs, cnt, sm, phase);
+                };
+                if (s0w > sw) {
+                    double A0, B0, k0;
+                    wsweep(s0w, A0, B0, k0);
+                    ++nsw;
+                    const double g0 = A0 + tw * B0 / s0w;
+                    if (g0 >= s0w) {
+                        sw = fmax(active_root(A0, B0, tw), s0w);
+                        prev = (int)k0;
+                    } else if (g0 > sw) {
+                        sw = g0;
+                        prev = -1;
+                    }
+                }
+                for (int k = 0; k < kMaxSweeps && !ok; ++k) {
+                    double As, Bs, kc;
+                    wsweep(sw, As, Bs, kc);
+                    ++nsw;
+                    const int cnt = (int)kc;
+                    if (cnt == prev || cnt == 0) {
+                        ok = cnt != 0 || h == 0;
+                        break;
+                    }
+                    sw = fmax(active_root(As, Bs, tw), sw);
+                    prev = cnt;
+                }
+                bool pass = false;
+                if (ok && h > 0) {
+                    const double th = (double)__int_as_float(hd.y), pm = (double)__int_as_float(hd.z);
+                    const double D = fmax(__dsub_ru(cnow, (double)__int_as_float(hd.w)), 0.0);
+                    const double lhs = __dmul_rd(__dmul_rd(th, sw), __dsub_rd(pm, D));
+                    const double rhs = __dmul_ru(__dmul_ru(wi, pm), 1.0 + MQ_WS_MARGIN);
+                    pass = lhs >= rhs && pm > D;
+                }
+                if (pass) {  // block-uniform
+                    const double inv_s = 1.0 / sw;
+                    for (int k = tid; k < h; k += T) {
+                        const double xn = fmax(s_c[k] + tw * s_u[k] * inv_s, 0.0);
+                        if (xn > 0.0 || s_f[k]) st.pl_x[po + k] = xn;
+                        put_x(mk, st, a + s_p[k], s_j[k], xn, s_f[k]);
+                    }
+                    if (tid == 0) {
+                        my_sweeps += nsw;
+                        st.srow[i] = sw;
+                    }
+                    continue;  // the next row (the loop head syncs)
+                }
+                __syncthreads();  // the full solve below reuses the shared arrays
+            }
+        }
         double s0 = 0.0, A = 0.0, B = 0.0;
         for (int k0 = tid; k0 < len; k0 += LB * T) {
             int jv[LB];
@@ -995,6 +1115,80 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
             st.srow[i] = s;
         }
         const double inv_s = 1.0 / s;
+        if (st.pl_hdr) {
+            // write-back fused with the working-set rebuild, chunk by chunk of
+            // T entries so the block scan ranks working entries in ascending
+            // position: nonzero entries and zero entries near the threshold
+            const int64_t po = r * (int64_t)CAP;
+            const double gw = MQ_WS_GAMMA * wi;
+            const int lane = tid & 31, warp = tid >> 5;
+            int base = 0;
+            double bp = CUDART_INF, bu = 1.0, pmn = CUDART_INF;
+            for (int k0 = 0; k0 < len; k0 += T) {
+                const int k = k0 + tid;
+                bool hot = false;
+                double ue = 0.0, xn = 0.0, pj = 0.0;
+                int j = 0;
+                if (k < len) {
+                    double ce;
+                    bool was;
+                    if (k < CAP) {
+                        ue = s_u[k];
+                        ce = s_c[k];
+                        j = s_j[k];
+                        was = s_f[k];
+                    } else {
+                        ue = __ldg(mk.u + a + k);
+                        ce = gx[k];
+                        j = __ldg(mk.col + a + k);
+                        was = true;  // the x slot held c: rewrite it
+                    }
+                    xn = fmax(ce + tw * ue * inv_s, 0.0);
+                    put_x(mk, st, a + k, j, xn, was);
+                    pj = __ldg(st.p + j);
+                    hot = xn > 0.0 || pj * s < gw * ue;
+                    if (!hot) {
+                        if (pj * bu < bp * ue) {
+                            bp = pj;
+                            bu = ue;
+                        }
+                        pmn = fmin(pmn, pj);
+                    }
+                }
+                const uint32_t bal = __ballot_sync(MQ_FULL, hot);
+                if (lane == 0) wtot[warp] = __popc(bal);
+                __syncthreads();
+                int before = 0, total = 0;
+                for (int q = 0; q < T / 32; ++q) {
+                    if (q < warp) before += wtot[q];
+                    total += wtot[q];
+                }
+                const int rank = base + before + __popc(bal & ((1u << lane) - 1u));
+                if (hot && rank < CAP) {
+                    st.pl_u[po + rank] = ue;
+                    st.pl_x[po + rank] = xn;
+                    st.pl_col[po + rank] = j;
+                    st.pl_pos[po + rank] = k;
+                }
+                base += total;
+                __syncthreads();  // wtot is rewritten by the next chunk
+            }
+            double th = bp == CUDART_INF ? CUDART_INF : __ddiv_rd(bp, bu) * (1.0 - 4e-16);
+            double dummy = 0.0;
+            th = -th;
+            pmn = -pmn;  // block max of the negatives = block min (fixed order)
+            block_max3(th, pmn, dummy, sm, phase);
+            th = -th;
+            pmn = -pmn;
+            if (tid == 0) {
+                reinterpret_cast<int4 *>(st.pl_hdr)[r] =
+                    base <= CAP ? make_int4(base, __float_as_int(__double2float_rd(th)),
+                                            __float_as_int(__double2float_rd(pmn)),
+                                            __float_as_int(__double2float_rd(cnow)))
+                                : make_int4(-2, 0, 0, 0);
+            }
+            continue;
+        }
         for (int k = tid; k < ns; k += T)
             put_x(mk, st, a + k, s_j[k], fmax(s_c[k] + tw * s_u[k] * inv_s, 0.0), s_f[k]);
         for (int k0 = CAP + tid; k0 < len; k0 += LB * T) {
@@ -1154,7 +1348,13 @@ struct WsStage {
     uint8_t pos[SB * K * 32];
 };
 using WsStageT = WsStage<MQ_WS_SLOTS, MQ_WS_SB>;
-constexpr int kWsSmem = MQ_WS_NST * (int)sizeof(WsStageT) + MQ_WS_NST * (2 * 8 + 8 + 4) + 64;
+#ifdef MQ_WS_CPASYNC
+constexpr int kWsGatherSmem = MQ_WS_NC * MQ_WS_SLOTS * 32 * 8;  // per-consumer gather slots
+#else
+constexpr int kWsGatherSmem = 0;
+#endif
+constexpr int kWsSmem =
+    MQ_WS_NST * (int)sizeof(WsStageT) + MQ_WS_NST * (2 * 8 + 8 + 4) + 64 + kWsGatherSmem;
 static_assert(sizeof(WsStageT) % 16 == 0, "stage must keep 16-byte alignment");
 
 __global__ void __launch_bounds__((MQ_WS_NC + 1) * 32, 1)
@@ -1272,6 +1472,12 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
         MQ_CHECK(h >= -3 && h <= K);
         if (force_full && h != -3) h = -1;
         uint32_t was = 0;  // slots whose x was nonzero
+#ifdef MQ_WS_CPASYNC
+        // the price gathers land in the warp's own shared-memory slots
+        // (cp.async): no registers held while they are in flight
+        double *pg = reinterpret_cast<double *>(wsm + NST * sizeof(WsStageT) + NST * (2 * 8 + 8 + 4) + 64) +
+                     warp * K * 32;
+#endif
 #pragma unroll
         for (int k = 0; k < K; ++k) {  // the price gathers leave before the release
             u[k] = 0.0;
@@ -1281,7 +1487,14 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
                 u[k] = d.u[so + k * 32];
                 c[k] = d.x[so + k * 32];
                 MQ_CHECK(d.col[so + k * 32] >= 0 && d.col[so + k * 32] < mk.m);
+#ifdef MQ_WS_CPASYNC
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                                 smem_addr(pg + k * 32 + lane)),
+                             "l"(st.p + d.col[so + k * 32])
+                             : "memory");
+#else
                 pv[k] = __ldg(st.p + d.col[so + k * 32]);
+#endif
                 if (c[k] > 0.0) was |= 1u << k;
             }
         }
@@ -1290,8 +1503,15 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
         if (!mine) continue;
         ws_push(st, h == -1 || h == -2, i);
         const bool act = h >= 0;
+#ifdef MQ_WS_CPASYNC
+        asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+            if (k < h) c[k] -= tau * pg[k * 32 + lane];
+#else
 #pragma unroll
         for (int k = 0; k < K; ++k) c[k] -= tau * pv[k];
+#endif
         const double tw = tau * w;
         // ---- exact root over the working set (row_root_warm, one thread)
         auto amask = [&](double z) -> uint32_t {
@@ -1789,6 +2009,7 @@ int mq_bucket_slots(void) { return 0; }  // no bucket mode in this build
 int mq_x_sparse(void) { return 1; }
 int mq_fixed_colsum(void) { return 1; }
 int mq_ws_slots(void) { return MQ_WS_SLOTS; }
+int mq_long_cap(void) { return MQ_LONG_CAP; }
 
 int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream) {
     const int grid = (int)((mk->m + 255) / 256);

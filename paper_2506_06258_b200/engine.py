@@ -286,6 +286,18 @@ class PdhcgEngine:
             self.ws_col = torch.zeros(ns, dtype=torch.int32, device=dev)
             self.ws_pos = torch.zeros(ns, dtype=torch.uint8, device=dev)
             self.ws_list = torch.zeros(max(1, dm.n), dtype=torch.int32, device=dev)
+            # long rows (> 1024 entries): one working-set pool of LONG_CAP
+            # entries per row, in dm.long_rows order
+            nl = int(dm.long_rows.numel())
+            self.pool = nl > 0
+            if self.pool:
+                C = nat.LONG_CAP
+                self.pl_hdr = torch.zeros(nl, 4, dtype=torch.int32, device=dev)
+                self.pl_hdr[:, 0] = -1
+                self.pl_u = torch.zeros(nl * C, **f64)
+                self.pl_x = torch.zeros(nl * C, **f64)
+                self.pl_col = torch.zeros(nl * C, dtype=torch.int32, device=dev)
+                self.pl_pos = torch.zeros(nl * C, dtype=torch.int32, device=dev)
             self.drift = torch.zeros(2, **f64)
         # fixed-point column sums: m u64 accumulators, zero between iterations
         fixed = getattr(getattr(dm, "lib", None), "mq_fixed_colsum", None)
@@ -348,6 +360,9 @@ class PdhcgEngine:
             for name in ("ws_hdr", "ws_kmax", "ws_u", "ws_x", "ws_col", "ws_pos", "ws_list",
                          "drift"):
                 setattr(s, name, getattr(self, name).data_ptr())
+            if self.pool:
+                for name in ("pl_hdr", "pl_u", "pl_x", "pl_col", "pl_pos"):
+                    setattr(s, name, getattr(self, name).data_ptr())
         s.navg = self.navg_dev.data_ptr()
         s.pass_out = self.pass_buf.data_ptr()
         return s
@@ -372,6 +387,8 @@ class PdhcgEngine:
         if self.working_set:
             self.ws_len.copy_(self.ws_init)
             self.ws_kmax.zero_()
+            if self.pool:
+                self.pl_hdr[:, 0] = -1
             self._rebuild = True
         if self.sparse:
             self.xflag.fill_(1)
@@ -462,6 +479,8 @@ class PdhcgEngine:
         if self.working_set:
             self.ws_len.copy_(self.ws_init)
             self.ws_kmax.zero_()
+            if self.pool:
+                self.pl_hdr[:, 0] = -1
             self._rebuild = True
 
     # ------------------------------------------------------------ chunks

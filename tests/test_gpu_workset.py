@@ -127,3 +127,38 @@ def test_solves_identical_with_and_without_working_sets(name):
     assert a.inner_iterations == b.inner_iterations == int(g["iters"])
     assert a.restarts == b.restarts == int(g["restarts"])
     assert np.max(np.abs(a.prices - b.prices) / np.abs(b.prices)) <= 1e-9
+
+
+def test_long_rows_solve_over_working_set_pools():
+    """Rows longer than 1024 entries (CTA per row) keep their working sets in
+    pools: after the first iterations most long rows have one, the pool
+    entries mirror (u, x, column, position) of the row, ascending, and hold
+    every nonzero entry."""
+    import torch
+
+    from paper_2506_06258_b200 import _native as nat
+
+    ws, _ = _pair(dict(n=60_000, m=8_000, powerlaw=2.0, mean_degree=40.0, seed=2))
+    assert ws.pool and ws.dm.long_rows.numel() > 10
+    ws.run_chunk(40)
+    ws.run_chunk(3)
+    torch.cuda.synchronize()
+    C = nat.LONG_CAP
+    hdr = ws.pl_hdr.cpu().numpy()
+    assert (hdr[:, 0] >= 0).mean() > 0.8
+    rp = ws.dm.row_ptr.cpu().numpy()
+    u, x, col = ws.dm.u.cpu().numpy(), ws.x.cpu().numpy(), ws.dm.col.cpu().numpy()
+    pu, px = ws.pl_u.cpu().numpy(), ws.pl_x.cpu().numpy()
+    pc, pp = ws.pl_col.cpu().numpy(), ws.pl_pos.cpu().numpy()
+    for r, i in enumerate(ws.dm.long_rows.cpu().numpy()):
+        h = hdr[r, 0]
+        if h < 0:
+            continue
+        pos = pp[r * C: r * C + h].astype(np.int64)
+        assert np.all(np.diff(pos) > 0)
+        g = rp[i] + pos
+        assert np.array_equal(pc[r * C: r * C + h], col[g])
+        assert np.array_equal(pu[r * C: r * C + h], u[g])
+        assert np.array_equal(px[r * C: r * C + h], x[g])
+        nz = np.nonzero(x[rp[i]:rp[i + 1]] > 0)[0]
+        assert set(nz.tolist()) <= set(pos.tolist())
