@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define MQ_ABI_VERSION 8
+#define MQ_ABI_VERSION 9
 #define MQ_TILE_ENTRIES 2560 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
@@ -163,6 +163,15 @@ typedef struct mq_state {
                          written every iteration)                           */
     int32_t *pl_col;  /* its good                                            */
     int32_t *pl_pos;  /* its offset in the row                               */
+    /* working sets of the medium rows longer than MQ_WS_MAX_ROW (the first
+       mk.nmed_long of mk.med_rows, the warp-per-row kernel; pm_hdr == NULL:
+       none), one pool of MQ_MED_CAP entries per row, laid out as pl_*      */
+    int32_t *pm_hdr;  /* [4 nmed_long] h (-1 none, -2 more than MQ_MED_CAP),
+                         theta, P, C                                        */
+    double *pm_u;     /* [nmed_long MQ_MED_CAP] normalized utility           */
+    double *pm_x;     /* its x (canonical x and flags also written)          */
+    int32_t *pm_col;  /* its good                                            */
+    int32_t *pm_pos;  /* its offset in the row                               */
     int32_t ws_rebuild; /* nonzero: this step runs the unscreened tile kernel
                            over every tile row and rebuilds all working sets
                            (after the host invalidated them; cheaper than
@@ -366,6 +375,8 @@ int mq_fixed_colsum(void);
 int mq_ws_slots(void);
 /* long-row working-set pool entries per row of this build (MQ_LONG_CAP) */
 int mq_long_cap(void);
+/* MQ_MED_CAP: entries of a medium row's working-set pool (mq_state.pm_*) */
+int mq_med_cap(void);
 /* 1 if the build keeps the sparse iterate (xflag / xsum) */
 int mq_x_sparse(void);
 /* sparse iterate: xbar = xsum / navg (call after mq_chunk_end) */

@@ -18,10 +18,11 @@ LONG_ROW = int(os.environ.get("MQ_LONG_ROW", "1024"))  # MQ_LONG_ROW (tuning ove
 REG_ROW = 128         # MQ_REG_ROW
 TILE_ROWS = 256       # MQ_TILE_ROWS
 PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
-ABI_VERSION = 8
+ABI_VERSION = 9
 WS_SLOTS = 12          # MQ_WS_SLOTS
 WS_MAX_ROW = 256       # MQ_WS_MAX_ROW
 LONG_CAP = 1536        # MQ_LONG_CAP (long-row working-set pool per row)
+MED_CAP = 128          # MQ_MED_CAP (medium-row working-set pool per row)
 
 _lock = threading.Lock()
 _lib = None
@@ -57,6 +58,7 @@ class MqState(ctypes.Structure):
                 ("xflag", P), ("xsum", P), ("ws_hdr", P), ("ws_kmax", P), ("ws_u", P),
                 ("ws_x", P), ("ws_col", P), ("ws_pos", P), ("ws_list", P), ("drift", P),
                 ("pl_hdr", P), ("pl_u", P), ("pl_x", P), ("pl_col", P), ("pl_pos", P),
+                ("pm_hdr", P), ("pm_u", P), ("pm_x", P), ("pm_col", P), ("pm_pos", P),
                 ("ws_rebuild", ctypes.c_int32)]
 
 
@@ -102,6 +104,7 @@ _SIGS = {
     "mq_x_sparse": (CINT, []),
     "mq_ws_slots": (CINT, []),
     "mq_long_cap": (CINT, []),
+    "mq_med_cap": (CINT, []),
     "mq_avg_materialize": (CINT, [PM, PS, P]),
     "mq_pdhg_step": (CINT, [PM, PL, CINT, P]),
     "mq_pdhg_colsum_only": (CINT, [PM, PL, CINT, P]),

@@ -75,6 +75,9 @@
 #ifndef MQ_LONG_LB
 #define MQ_LONG_LB 4  // entries per thread batched ahead of the stores (long rows)
 #endif
+#ifndef MQ_MED_CAP
+#define MQ_MED_CAP 128  // working-set pool of a medium row > MQ_WS_MAX_ROW (4 per lane)
+#endif
 #ifndef MQ_LONG_CAP
 #define MQ_LONG_CAP 1536  // entries of a long row kept in shared memory (32 KB, 4 CTAs/SM:
                           // the rest of the carveout stays L1 for the price gathers)
@@ -1232,9 +1235,10 @@ __global__ void __launch_bounds__(256)
 #endif
 primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
                   int64_t nrows) {
-    constexpr int G = 32, LB = MQ_MED_LB;
+    constexpr int G = 32, LB = MQ_MED_LB, PC = MQ_MED_CAP / G;
     const double tau = st.steps[0];
     const int lane = threadIdx.x & 31;
+    const double cnow = st.pm_hdr ? drift_now(st) : 0.0;
     int my_sweeps = 0, my_faults = 0;
     for (;;) {
         int r = 0;
@@ -1246,11 +1250,64 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
         const int64_t e0 = mk.row_ptr[i];
         const int len = (int)(mk.row_ptr[i + 1] - e0);
         MQ_CHECK(e0 >= 0 && e0 + len <= mk.nnz);
-        const double tw = tau * mk.w[i];
+        const double wi = mk.w[i];
+        const double tw = tau * wi;
         const double *__restrict__ su = mk.u + e0;
         const int32_t *__restrict__ cl = mk.col + e0;
         const uint8_t *__restrict__ fl = st.xflag + e0;
         double *sc = st.x + e0;
+        // rows longer than MQ_WS_MAX_ROW have a pool (the leading nmed_long)
+        const bool pooled = st.pm_hdr != nullptr && r < mk.nmed_long;
+        const int64_t po = r * (int64_t)MQ_MED_CAP;
+        if (pooled && !x_prev_out) {
+            // screened solve over the pool, in registers; the certificate of
+            // the short rows
+            const int4 hd = reinterpret_cast<const int4 *>(st.pm_hdr)[r];
+            const int h = hd.x;
+            MQ_CHECK(h >= -2 && h <= MQ_MED_CAP);
+            if (h > 0) {
+                double c[PC], u[PC], xk[PC];
+                int jc[PC], ps[PC];
+#pragma unroll
+                for (int e = 0; e < PC; ++e) {
+                    const int k = lane + e * G;
+                    const bool in = k < h;
+                    u[e] = in ? __ldcg(st.pm_u + po + k) : 0.0;
+                    xk[e] = in ? __ldcg(st.pm_x + po + k) : 0.0;
+                    jc[e] = in ? __ldcg(st.pm_col + po + k) : 0;
+                    ps[e] = in ? __ldcg(st.pm_pos + po + k) : 0;
+                    MQ_CHECK(!in || (jc[e] >= 0 && jc[e] < mk.m && ps[e] >= 0 && ps[e] < len));
+                }
+#pragma unroll
+                for (int e = 0; e < PC; ++e)
+                    c[e] = xk[e] - tau * (lane + e * G < h ? __ldg(st.p + jc[e]) : 0.0);
+                int nsw = 0;
+                bool ok = true;
+                const double sw = row_root_warm<G, PC>(c, u, tw, st.srow[i], true, MQ_FULL, &nsw, &ok);
+                const double th = (double)__int_as_float(hd.y), pm = (double)__int_as_float(hd.z);
+                const double D = fmax(__dsub_ru(cnow, (double)__int_as_float(hd.w)), 0.0);
+                const double lhs = __dmul_rd(__dmul_rd(th, sw), __dsub_rd(pm, D));
+                const double rhs = __dmul_ru(__dmul_ru(wi, pm), 1.0 + MQ_WS_MARGIN);
+                if (ok && lhs >= rhs && pm > D) {  // warp-uniform
+                    const double inv_s = 1.0 / sw;
+#pragma unroll
+                    for (int e = 0; e < PC; ++e) {
+                        const int k = lane + e * G;
+                        if (k < h) {
+                            const double xn = fmax(c[e] + tw * u[e] * inv_s, 0.0);
+                            const bool was = xk[e] > 0.0;
+                            if (xn > 0.0 || was) st.pm_x[po + k] = xn;
+                            put_x(mk, st, e0 + ps[e], jc[e], xn, was);
+                        }
+                    }
+                    if (lane == 0) {
+                        st.srow[i] = sw;
+                        my_sweeps += nsw;
+                    }
+                    continue;
+                }
+            }
+        }
         double s0p = 0.0, ap = 0.0, bp = 0.0;
         for (int t0 = lane; t0 < len; t0 += LB * G) {
             double pv[LB], xv[LB], uv[LB];
@@ -1287,6 +1344,63 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
             if (!ok) ++my_faults;
         }
         const double inv_s = 1.0 / sr;
+        if (pooled) {
+            // write-back fused with the pool rebuild: warp-wide chunks of 32
+            // entries in ascending position, ballots rank the working entries
+            // (nonzero, or zero with p_j s < gamma w u_j)
+            const double gw = MQ_WS_GAMMA * wi;
+            int base = 0;
+            double bp = CUDART_INF, bu = 1.0, pmn = CUDART_INF;
+            for (int b0 = 0; b0 < len; b0 += LB * G) {  // warp-uniform bounds
+                double cv[LB], uv[LB], pv[LB];
+                int jv[LB];
+#pragma unroll
+                for (int q = 0; q < LB; ++q) {
+                    const int t = b0 + q * G + lane;
+                    const bool in = t < len;
+                    cv[q] = in ? sc[t] : 0.0;
+                    uv[q] = in ? __ldg(su + t) : 0.0;
+                    jv[q] = in ? __ldg(cl + t) : 0;
+                }
+#pragma unroll
+                for (int q = 0; q < LB; ++q)
+                    pv[q] = b0 + q * G + lane < len ? __ldg(st.p + jv[q]) : 0.0;
+#pragma unroll
+                for (int q = 0; q < LB; ++q) {
+                    const int t = b0 + q * G + lane;
+                    const bool in = t < len;
+                    const double xn = in ? fmax(cv[q] + tw * uv[q] * inv_s, 0.0) : 0.0;
+                    if (in) put_x(mk, st, e0 + t, jv[q], xn, true);  // x held c
+                    const bool hot = in && (xn > 0.0 || pv[q] * sr < gw * uv[q]);
+                    if (in && !hot) {
+                        if (pv[q] * bu < bp * uv[q]) {
+                            bp = pv[q];
+                            bu = uv[q];
+                        }
+                        pmn = fmin(pmn, pv[q]);
+                    }
+                    const uint32_t bal = __ballot_sync(MQ_FULL, hot);
+                    const int rank = base + __popc(bal & ((1u << lane) - 1u));
+                    if (hot && rank < MQ_MED_CAP) {
+                        st.pm_u[po + rank] = uv[q];
+                        st.pm_x[po + rank] = xn;
+                        st.pm_col[po + rank] = jv[q];
+                        st.pm_pos[po + rank] = t;
+                    }
+                    base += __popc(bal);
+                }
+            }
+            double th = bp == CUDART_INF ? CUDART_INF : __ddiv_rd(bp, bu) * (1.0 - 4e-16);
+            th = group_min<32>(th);
+            pmn = group_min<32>(pmn);
+            if (lane == 0)
+                reinterpret_cast<int4 *>(st.pm_hdr)[r] =
+                    base <= MQ_MED_CAP ? make_int4(base, __float_as_int(__double2float_rd(th)),
+                                                   __float_as_int(__double2float_rd(pmn)),
+                                                   __float_as_int(__double2float_rd(cnow)))
+                                       : make_int4(-2, 0, 0, 0);
+            continue;
+        }
         for (int t0 = lane; t0 < len; t0 += LB * G) {
             double cv[LB], uv[LB];
             int jv[LB];
@@ -2010,6 +2124,7 @@ int mq_x_sparse(void) { return 1; }
 int mq_fixed_colsum(void) { return 1; }
 int mq_ws_slots(void) { return MQ_WS_SLOTS; }
 int mq_long_cap(void) { return MQ_LONG_CAP; }
+int mq_med_cap(void) { return MQ_MED_CAP; }
 
 int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream) {
     const int grid = (int)((mk->m + 255) / 256);

@@ -298,6 +298,18 @@ class PdhcgEngine:
                 self.pl_x = torch.zeros(nl * C, **f64)
                 self.pl_col = torch.zeros(nl * C, dtype=torch.int32, device=dev)
                 self.pl_pos = torch.zeros(nl * C, dtype=torch.int32, device=dev)
+            # medium rows longer than WS_MAX_ROW (the leading nmed_long of
+            # dm.med_rows): a pool of MED_CAP entries each
+            nml = int(dm.struct.nmed_long) if dm.struct.nmed else 0
+            self.mpool = nml > 0
+            if self.mpool:
+                C = nat.MED_CAP
+                self.pm_hdr = torch.zeros(nml, 4, dtype=torch.int32, device=dev)
+                self.pm_hdr[:, 0] = -1
+                self.pm_u = torch.zeros(nml * C, **f64)
+                self.pm_x = torch.zeros(nml * C, **f64)
+                self.pm_col = torch.zeros(nml * C, dtype=torch.int32, device=dev)
+                self.pm_pos = torch.zeros(nml * C, dtype=torch.int32, device=dev)
             self.drift = torch.zeros(2, **f64)
         # fixed-point column sums: m u64 accumulators, zero between iterations
         fixed = getattr(getattr(dm, "lib", None), "mq_fixed_colsum", None)
@@ -363,6 +375,9 @@ class PdhcgEngine:
             if self.pool:
                 for name in ("pl_hdr", "pl_u", "pl_x", "pl_col", "pl_pos"):
                     setattr(s, name, getattr(self, name).data_ptr())
+            if self.mpool:
+                for name in ("pm_hdr", "pm_u", "pm_x", "pm_col", "pm_pos"):
+                    setattr(s, name, getattr(self, name).data_ptr())
         s.navg = self.navg_dev.data_ptr()
         s.pass_out = self.pass_buf.data_ptr()
         return s
@@ -389,6 +404,8 @@ class PdhcgEngine:
             self.ws_kmax.zero_()
             if self.pool:
                 self.pl_hdr[:, 0] = -1
+            if self.mpool:
+                self.pm_hdr[:, 0] = -1
             self._rebuild = True
         if self.sparse:
             self.xflag.fill_(1)
@@ -481,6 +498,8 @@ class PdhcgEngine:
             self.ws_kmax.zero_()
             if self.pool:
                 self.pl_hdr[:, 0] = -1
+            if self.mpool:
+                self.pm_hdr[:, 0] = -1
             self._rebuild = True
 
     # ------------------------------------------------------------ chunks

@@ -129,6 +129,26 @@ def test_solves_identical_with_and_without_working_sets(name):
     assert np.max(np.abs(a.prices - b.prices) / np.abs(b.prices)) <= 1e-9
 
 
+def _check_pools(eng, rows, hdr, pu, px, pc, pp, C):
+    """Every valid pool mirrors (u, x, column, position) of its row in
+    ascending position and holds each nonzero entry."""
+    rp = eng.dm.row_ptr.cpu().numpy()
+    u, x, col = eng.dm.u.cpu().numpy(), eng.x.cpu().numpy(), eng.dm.col.cpu().numpy()
+    pu, px, pc, pp = (t.cpu().numpy() for t in (pu, px, pc, pp))
+    for r, i in enumerate(rows):
+        h = hdr[r, 0]
+        if h < 0:
+            continue
+        pos = pp[r * C: r * C + h].astype(np.int64)
+        assert np.all(np.diff(pos) > 0)
+        g = rp[i] + pos
+        assert np.array_equal(pc[r * C: r * C + h], col[g])
+        assert np.array_equal(pu[r * C: r * C + h], u[g])
+        assert np.array_equal(px[r * C: r * C + h], x[g])
+        nz = np.nonzero(x[rp[i]:rp[i + 1]] > 0)[0]
+        assert set(nz.tolist()) <= set(pos.tolist())
+
+
 def test_long_rows_solve_over_working_set_pools():
     """Rows longer than 1024 entries (CTA per row) keep their working sets in
     pools: after the first iterations most long rows have one, the pool
@@ -143,22 +163,27 @@ def test_long_rows_solve_over_working_set_pools():
     ws.run_chunk(40)
     ws.run_chunk(3)
     torch.cuda.synchronize()
-    C = nat.LONG_CAP
     hdr = ws.pl_hdr.cpu().numpy()
     assert (hdr[:, 0] >= 0).mean() > 0.8
-    rp = ws.dm.row_ptr.cpu().numpy()
-    u, x, col = ws.dm.u.cpu().numpy(), ws.x.cpu().numpy(), ws.dm.col.cpu().numpy()
-    pu, px = ws.pl_u.cpu().numpy(), ws.pl_x.cpu().numpy()
-    pc, pp = ws.pl_col.cpu().numpy(), ws.pl_pos.cpu().numpy()
-    for r, i in enumerate(ws.dm.long_rows.cpu().numpy()):
-        h = hdr[r, 0]
-        if h < 0:
-            continue
-        pos = pp[r * C: r * C + h].astype(np.int64)
-        assert np.all(np.diff(pos) > 0)
-        g = rp[i] + pos
-        assert np.array_equal(pc[r * C: r * C + h], col[g])
-        assert np.array_equal(pu[r * C: r * C + h], u[g])
-        assert np.array_equal(px[r * C: r * C + h], x[g])
-        nz = np.nonzero(x[rp[i]:rp[i + 1]] > 0)[0]
-        assert set(nz.tolist()) <= set(pos.tolist())
+    _check_pools(ws, ws.dm.long_rows.cpu().numpy(), hdr, ws.pl_u, ws.pl_x, ws.pl_col,
+                 ws.pl_pos, nat.LONG_CAP)
+
+
+def test_medium_rows_solve_over_working_set_pools():
+    """Rows of 257-1024 entries (warp per row) keep their working sets in
+    pools of MED_CAP entries, with the same invariants as the long rows'."""
+    import torch
+
+    from paper_2506_06258_b200 import _native as nat
+
+    assert nat.lib().mq_med_cap() == nat.MED_CAP
+    ws, _ = _pair(dict(n=60_000, m=8_000, powerlaw=2.0, mean_degree=40.0, seed=2))
+    nml = int(ws.dm.struct.nmed_long)
+    assert ws.mpool and nml > 100
+    ws.run_chunk(40)
+    ws.run_chunk(3)
+    torch.cuda.synchronize()
+    hdr = ws.pm_hdr.cpu().numpy()
+    assert hdr.shape[0] == nml and (hdr[:, 0] >= 0).mean() > 0.8
+    _check_pools(ws, ws.dm.med_rows[:nml].cpu().numpy(), hdr, ws.pm_u, ws.pm_x, ws.pm_col,
+                 ws.pm_pos, nat.MED_CAP)
