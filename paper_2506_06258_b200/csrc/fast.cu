@@ -1439,13 +1439,13 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
 // (left side down, right side up).  Rows without a working set, or whose
 // certificate fails, go to the full-solve list untouched.
 #ifndef MQ_WS_NC
-#define MQ_WS_NC 15  // consumer warps per CTA (one CTA per SM; 16 warps: <= 128 registers)
+#define MQ_WS_NC 11  // consumer warps per CTA (one CTA per SM; 12 warps: <= 168 registers)
 #endif
 #ifndef MQ_WS_SB
-#define MQ_WS_SB 4  // 32-row blocks per stage
+#define MQ_WS_SB 8  // 32-row blocks per stage
 #endif
 #ifndef MQ_WS_NST
-#define MQ_WS_NST 4  // stages
+#define MQ_WS_NST 2  // stages
 #endif
 template <int K, int SB>
 struct WsStage {
@@ -1474,6 +1474,7 @@ static_assert(sizeof(WsStageT) % 16 == 0, "stage must keep 16-byte alignment");
 __global__ void __launch_bounds__((MQ_WS_NC + 1) * 32, 1)
 ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
     constexpr int K = MQ_WS_SLOTS, SB = MQ_WS_SB, NST = MQ_WS_NST, NC = MQ_WS_NC;
+    static_assert(SB <= NC, "every warp takes at most one block per stage visit");
     extern __shared__ __align__(128) unsigned char wsm[];
     WsStageT *stg = reinterpret_cast<WsStageT *>(wsm);
     uint64_t *full = reinterpret_cast<uint64_t *>(wsm + NST * sizeof(WsStageT));

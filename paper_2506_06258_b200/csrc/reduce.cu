@@ -122,8 +122,19 @@ resid_rows_kernel(const mq_market mk, const double *__restrict__ x, double2 *__r
 // slot per good holds (p, its column max, pbar, its column max), so an entry
 // costs one random sector for both.  Same row assignment, lane sums and
 // block partials as resid_rows_kernel: bitwise the two separate passes.
+#ifndef MQ_RP_MINB
+#define MQ_RP_MINB 3  // resident 256-thread CTAs per SM of the fused residual pass
+#endif
+#ifndef MQ_RP_LB
+#define MQ_RP_LB 2  // entries per lane batched ahead of the atomics
+#endif
+#ifndef MQ_RP_GRID
+#define MQ_RP_GRID 444  // CTAs of the residual row passes: 3 per SM on 148 SMs; fixes the
+                        // order of the objective's block partials (C4 sweep, DESIGN.md §11:
+                        // 2/4/1024 -> 12.7 ms, 3/2/444 -> 10.2 ms per check)
+#endif
 template <int G>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, MQ_RP_MINB)
 resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
                   const uint8_t *__restrict__ xflag, const double *__restrict__ xbar,
                   double4 *__restrict__ pc4, double *__restrict__ sa, double *__restrict__ sb) {
@@ -172,7 +183,7 @@ resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
         if (!ok[0] && !ok[1]) continue;
         // LB entries per lane per batch: every load of the batch (and its
         // price-slot gather) is issued before the atomics that consume them
-        constexpr int LB = 4;
+        constexpr int LB = MQ_RP_LB;
         for (int64_t t0 = a + lane; t0 < b; t0 += LB * G) {
             int32_t jv[LB];
             double uv[LB], xv[LB], bv[LB];
@@ -189,8 +200,14 @@ resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
             }
 #pragma unroll
             for (int q = 0; q < LB; ++q) {
+#ifdef MQ_RESID_LD2  // two 16-byte loads of the slot (the earlier form)
                 q01[q] = __ldcg(reinterpret_cast<const double2 *>(pc4 + jv[q]));
                 q23[q] = __ldcg(reinterpret_cast<const double2 *>(pc4 + jv[q]) + 1);
+#else  // one 32-byte load (sm_100 LDG.256): one L2 request per entry
+                asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                             : "=d"(q01[q].x), "=d"(q01[q].y), "=d"(q23[q].x), "=d"(q23[q].y)
+                             : "l"(pc4 + jv[q]));
+#endif
             }
 #pragma unroll
             for (int q = 0; q < LB; ++q) {
@@ -403,7 +420,7 @@ int mq_resid_rows(const mq_market *mk, const double *x, const double *p, int use
                   double *colbest, double *work, double *t_out, double *y_out, double *row_out,
                   double *scratch, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    const int grid = grid_for(mk->n, 8, MQ_MAX_BLOCKS);
+    const int grid = grid_for(mk->n, 8, MQ_RP_GRID);
     cudaMemsetAsync(scratch + kMisc, 0, 4 * sizeof(double), s);
     cudaMemsetAsync(scratch + kMisc + 4, 0xff, sizeof(double), s);
     double2 *pc = reinterpret_cast<double2 *>(work);
@@ -428,7 +445,7 @@ int mq_resid_rows_pair(const mq_market *mk, const mq_state *st, double *colbest_
                        void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (!mk || !st || !work) return set_error(cudaErrorInvalidValue, "mq_resid_rows_pair: null");
-    const int grid = grid_for(mk->n, 8, MQ_MAX_BLOCKS);
+    const int grid = grid_for(mk->n, 8, MQ_RP_GRID);
     for (double *sc : {scratch_last, scratch_avg}) {
         cudaMemsetAsync(sc + kMisc, 0, 4 * sizeof(double), s);
         cudaMemsetAsync(sc + kMisc + 4, 0xff, sizeof(double), s);
