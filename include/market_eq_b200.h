@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define MQ_ABI_VERSION 9
+#define MQ_ABI_VERSION 10
 #define MQ_TILE_ENTRIES 2560 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
@@ -176,6 +176,10 @@ typedef struct mq_state {
                            over every tile row and rebuilds all working sets
                            (after the host invalidated them; cheaper than
                            the per-row full solves when every row needs one) */
+    int32_t xbar_lazy;  /* nonzero: xbar is stale (the host skipped
+                           mq_avg_xbar after the last chunk);
+                           mq_resid_rows_pair reads the average as
+                           xsum / navg instead                               */
 } mq_state;
 
 /* Mutable iterate of the lifted PDHG path (algo="pdhg", kernels.py:146-197):
@@ -379,7 +383,11 @@ int mq_long_cap(void);
 int mq_med_cap(void);
 /* 1 if the build keeps the sparse iterate (xflag / xsum) */
 int mq_x_sparse(void);
-/* sparse iterate: xbar = xsum / navg (call after mq_chunk_end) */
+/* sparse iterate, after mq_chunk_end: the screened rows' x and flags from
+ * their working-set slots (mq_ws_flush), then xbar = xsum / navg
+ * (mq_avg_xbar); mq_avg_materialize runs both */
+int mq_ws_flush(const mq_market *mk, const mq_state *st, void *stream);
+int mq_avg_xbar(const mq_market *mk, const mq_state *st, void *stream);
 int mq_avg_materialize(const mq_market *mk, const mq_state *st, void *stream);
 
 #ifdef __cplusplus

@@ -2085,14 +2085,24 @@ int mq_chunk_end(const mq_state *st, int iters, void *stream) {
     return check_launch("mq_chunk_end");
 }
 
-int mq_avg_materialize(const mq_market *mk, const mq_state *st, void *stream) {
-    if (!mk || !st) return set_error(cudaErrorInvalidValue, "mq_avg_materialize: null argument");
+int mq_ws_flush(const mq_market *mk, const mq_state *st, void *stream) {
+    if (!mk || !st) return set_error(cudaErrorInvalidValue, "mq_ws_flush: null argument");
     if (st->ws_hdr)  // the screened rows' x and flags, from their slots
         ws_flush_kernel<<<grid_for(mk->n, 256, sm_count() * 16), 256, 0, (cudaStream_t)stream>>>(
             mk->n, mk->row_ptr, *st);
+    return check_launch("mq_ws_flush");
+}
+
+int mq_avg_xbar(const mq_market *mk, const mq_state *st, void *stream) {
+    if (!mk || !st) return set_error(cudaErrorInvalidValue, "mq_avg_xbar: null argument");
     avg_materialize_kernel<<<grid_for(mk->nnz, 256, sm_count() * 16), 256, 0,
                              (cudaStream_t)stream>>>(mk->nnz, st->xsum, st->xbar, st->navg);
-    return check_launch("mq_avg_materialize");
+    return check_launch("mq_avg_xbar");
+}
+
+int mq_avg_materialize(const mq_market *mk, const mq_state *st, void *stream) {
+    if (int rc = mq_ws_flush(mk, st, stream)) return rc;
+    return mq_avg_xbar(mk, st, stream);
 }
 
 int mq_fast_chunk(const mq_market *mk, const mq_state *st, int iters, void *stream) {

@@ -137,8 +137,16 @@ template <int G>
 __global__ void __launch_bounds__(256, MQ_RP_MINB)
 resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
                   const uint8_t *__restrict__ xflag, const double *__restrict__ xbar,
+                  const double *__restrict__ xsum, const int64_t *__restrict__ navg,
                   double4 *__restrict__ pc4, double *__restrict__ sa, double *__restrict__ sb) {
     const double *__restrict__ U = mk.u_orig;
+    // xsum != NULL: the average is read as xsum / navg, bit for bit what
+    // avg_materialize_kernel would store (one reciprocal, one product)
+    const double cnt = xsum ? (double)*navg : 0.0;
+    const bool lazy = cnt > 0.0;
+    const double inv = lazy ? 1.0 / cnt : 0.0;
+    const double *__restrict__ xb = lazy ? xsum : xbar;
+    const double sc = lazy ? inv : 1.0;
     constexpr int RPW = 32 / G;
     const int lane = threadIdx.x & (G - 1);
     const int gsub = (threadIdx.x & 31) / G;
@@ -159,7 +167,7 @@ resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
         for (int64_t t = a + lane; t < b; t += G) {
             const double ut = U[t];
             if (xflag[t]) tp += ut * x[t];  // zero entries add +0.0 exactly
-            tq += ut * xbar[t];
+            tq += ut * (xb[t] * sc);
         }
         const double ti[2] = {group_sum<G>(tp), group_sum<G>(tq)};
         bool ok[2];
@@ -196,7 +204,7 @@ resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
                 MQ_CHECK(jv[q] >= 0 && jv[q] < mk.m);
                 uv[q] = in ? U[t] : 0.0;
                 xv[q] = (in && xflag[t]) ? x[t] : 0.0;
-                bv[q] = in ? xbar[t] : 0.0;
+                bv[q] = in ? xb[t] * sc : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < LB; ++q) {
@@ -453,7 +461,9 @@ int mq_resid_rows_pair(const mq_market *mk, const mq_state *st, double *colbest_
     double4 *pc4 = reinterpret_cast<double4 *>(work);
     const int gm = grid_for(mk->m, 256, MQ_MAX_BLOCKS);
     pc4_init_kernel<<<gm, 256, 0, s>>>(mk->m, st->p, st->pbar, pc4);
-    resid_pair_kernel<8><<<grid, 256, 0, s>>>(*mk, st->x, st->xflag, st->xbar, pc4, scratch_last,
+    resid_pair_kernel<8><<<grid, 256, 0, s>>>(*mk, st->x, st->xflag, st->xbar,
+                                              st->xbar_lazy ? st->xsum : nullptr, st->navg,
+                                              pc4, scratch_last,
                                               scratch_avg);
     pc4_out_kernel<<<gm, 256, 0, s>>>(mk->m, pc4, colbest_last, colbest_avg);
     sum_slots_kernel<<<1, 64, 0, s>>>(scratch_last, grid, 2, scratch_last + kMisc + 16);

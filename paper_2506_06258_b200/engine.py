@@ -161,9 +161,13 @@ class NativeOps:
 
     def chunk_end(self, iters):
         self._c(self.lib.mq_chunk_end(self.eng.state, iters, _cur_stream()), "mq_chunk_end")
-        if self.eng.sparse:
-            self._c(self.lib.mq_avg_materialize(self.dm.struct, self.eng.state, _cur_stream()),
-                    "mq_avg_materialize")
+        if self.eng.sparse:  # x from the slots; xbar is formed on demand (PdhcgEngine.xbar)
+            self._c(self.lib.mq_ws_flush(self.dm.struct, self.eng.state, _cur_stream()),
+                    "mq_ws_flush")
+
+    def avg_xbar(self):
+        self._c(self.lib.mq_avg_xbar(self.dm.struct, self.eng.state, _cur_stream()),
+                "mq_avg_xbar")
 
     def resid_rows(self, x, p, use_norm, colbest, t_out, out, scratch):
         work = self.eng.resid_work
@@ -247,7 +251,8 @@ class PdhcgEngine:
         self._x_buf = torch.zeros(nnz + nat.PAD, **f64)
         self._xbar_buf = torch.zeros(nnz + nat.PAD, **f64)
         self.x = self._x_buf[:nnz]
-        self.xbar = self._xbar_buf[:nnz]
+        self._xbar_t = self._xbar_buf[:nnz]
+        self._xbar_stale = False  # sparse iterate: xbar not yet formed from xsum
         self.x0 = torch.zeros(nnz, **f64)
         # sparse iterate: x > 0 flags and the running sum of x
         self.sparse = bool(hasattr(dm, "lib") and dm.lib.mq_x_sparse() == 1
@@ -532,6 +537,7 @@ class PdhcgEngine:
             self._launch_chunk(iters, rebuild)
         self._rebuild = False
         self.navg += iters
+        self._xbar_stale = self.sparse
         vals = torch.cat([self.pass_buf[:iters], self.faults]).cpu().numpy()
         if vals[-1]:
             raise FixedPointRangeError(
@@ -634,13 +640,28 @@ class PdhcgEngine:
         return Residuals(float(r_primal), float(r_dual), float(r_gap),
                          float(max(r_primal, r_dual, r_gap)))
 
+    @property
+    def xbar(self):
+        """The running average x̄.  With the sparse iterate a chunk leaves it
+        as xsum / navg unformed (the residual check reads the sum directly);
+        it is formed here, once, when anything else reads it."""
+        if self._xbar_stale:
+            self._xbar_stale = False
+            self.ops.avg_xbar()
+        return self._xbar_t
+
     def residuals_pair(self):
         """(last, avg) residuals on the ORIGINAL instance with one sync; with
-        the sparse iterate both row passes run as one sweep (mq_resid_rows_pair)."""
+        the sparse iterate both row passes run as one sweep (mq_resid_rows_pair),
+        reading x̄ as xsum / navg when it has not been formed."""
         if self.sparse and isinstance(self.ops, NativeOps):
             self.colbest.zero_()
-            self.ops.resid_pair(self.colbest[0], self.colbest[1], self.out[0:8],
-                                self.out[16:24])
+            self.state.xbar_lazy = int(self._xbar_stale)
+            try:
+                self.ops.resid_pair(self.colbest[0], self.colbest[1], self.out[0:8],
+                                    self.out[16:24])
+            finally:
+                self.state.xbar_lazy = 0
             self._reduce_rows(0)
             self._reduce_rows(1)
         else:

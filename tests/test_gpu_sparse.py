@@ -97,7 +97,9 @@ def test_restart_resets_the_running_sum():
 def test_fused_residual_pair_is_bitwise_the_two_passes():
     """mq_resid_rows_pair (one sweep for the last and the averaged iterate)
     against the two separate mq_resid_rows passes, mid-solve on a generated
-    market with medium rows: identical residuals and column maxima."""
+    market with medium rows: identical residuals and column maxima.  The
+    fused sweep runs before x̄ is formed (it reads xsum / navg), the separate
+    passes after: the lazy average is bit for bit the formed one."""
     import torch
 
     from paper_2506_06258_b200.device import DeviceMarket
@@ -110,7 +112,9 @@ def test_fused_residual_pair_is_bitwise_the_two_passes():
     eng.set_steps(0.05, 0.05)
     for _ in range(3):
         eng.run_chunk(40)
+    assert eng._xbar_stale
     fused = eng.residuals_pair()
+    assert eng._xbar_stale
     out_f, cb_f = eng.out.clone(), eng.colbest.clone()
     eng._rows(eng.x, eng.p, 0, 0)
     eng._cols(eng.cs, eng.p, 0)
