@@ -1542,10 +1542,20 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
                     const int64_t o = (b0 + e) * K * 32;
                     const int so = e * K * 32;
                     const uint32_t ns = (uint32_t)km[e] * 32u;
-                    bulk_g2s_hint(d.u + so, st.ws_u + o, ns * 8u, &full[q], pol);
-                    bulk_g2s_hint(d.x + so, st.ws_x + o, ns * 8u, &full[q], pol);
-                    bulk_g2s_hint(d.col + so, st.ws_col + o, ns * 4u, &full[q], pol);
-                    bulk_g2s_hint(d.pos + so, st.ws_pos + o, ns, &full[q], pol);
+#ifndef MQ_WS_HINT
+#define MQ_WS_HINT 1  // bit 0: u, bit 1: x, bit 2: col and pos copied evict-first
+#endif
+                    if (MQ_WS_HINT & 1) bulk_g2s_hint(d.u + so, st.ws_u + o, ns * 8u, &full[q], pol);
+                    else bulk_g2s(d.u + so, st.ws_u + o, ns * 8u, &full[q]);
+                    if (MQ_WS_HINT & 2) bulk_g2s_hint(d.x + so, st.ws_x + o, ns * 8u, &full[q], pol);
+                    else bulk_g2s(d.x + so, st.ws_x + o, ns * 8u, &full[q]);
+                    if (MQ_WS_HINT & 4) {
+                        bulk_g2s_hint(d.col + so, st.ws_col + o, ns * 4u, &full[q], pol);
+                        bulk_g2s_hint(d.pos + so, st.ws_pos + o, ns, &full[q], pol);
+                    } else {  // re-read by the write-back: keep them in L2
+                        bulk_g2s(d.col + so, st.ws_col + o, ns * 4u, &full[q]);
+                        bulk_g2s(d.pos + so, st.ws_pos + o, ns, &full[q]);
+                    }
                 }
             }
         }
