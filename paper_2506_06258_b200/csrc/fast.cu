@@ -1709,12 +1709,13 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
             for (int k = 0; k < K; ++k)
                 if (k < h && c[k] + tw * u[k] * inv_s > 0.0) wm |= 1u << k;
             int pos[K], jc[K];
+            const int64_t wb = ws_at(i, 0);  // slot k at wb + 32 k
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 pos[k] = 0;
                 jc[k] = 0;
                 if ((wm >> k) & 1u) {
-                    const int64_t at = ws_at(i, k);
+                    const int64_t at = wb + (k << 5);
                     pos[k] = __ldcg(st.ws_pos + at);
                     jc[k] = __ldcg(st.ws_col + at);
                     MQ_CHECK(e0 + pos[k] < mk.nnz && jc[k] >= 0 && jc[k] < mk.m);
@@ -1726,7 +1727,7 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
                     // the slot is authoritative; x and its flag are written
                     // back once per chunk (ws_flush_kernel)
                     const double xn = fmax(c[k] + tw * u[k] * inv_s, 0.0);
-                    st.ws_x[ws_at(i, k)] = xn;
+                    st.ws_x[wb + (k << 5)] = xn;
                     if (xn > 0.0) {
                         red_add_f64(st.xsum + e0 + pos[k], xn);
                         fixed_colsum_add(mk, st, jc[k], xn);
