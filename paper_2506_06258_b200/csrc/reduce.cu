@@ -48,7 +48,7 @@ template <int G>
 __global__ void __launch_bounds__(256)
 resid_rows_kernel(const mq_market mk, const double *__restrict__ x, double2 *__restrict__ pc,
                   int use_norm, double *__restrict__ t_out, double *__restrict__ y_out,
-                  double *__restrict__ scratch) {
+                  double *__restrict__ scratch, int skip_long) {
     const double *__restrict__ U = use_norm ? mk.u : mk.u_orig;
     constexpr int RPW = 32 / G;  // rows per warp
     const int lane = threadIdx.x & (G - 1);
@@ -59,11 +59,15 @@ resid_rows_kernel(const mq_market mk, const double *__restrict__ x, double2 *__r
     double ymax = 0.0, gmax = 0.0, xmax = 0.0, emax = 0.0, obj = 0.0, nbad = 0.0;
     for (int64_t base = warp_id * RPW; base < mk.n; base += nwarps * RPW) {
         const int64_t i = base + gsub;
-        const bool has = i < mk.n;
+        bool has = i < mk.n;
         int64_t a = 0, b = 0;
         if (has) {
             a = mk.row_ptr[i];
             b = mk.row_ptr[i + 1];
+        }
+        if (has && skip_long && b - a > MQ_LONG_ROW) {  // resid_rows_long_kernel's row
+            has = false;
+            b = a;
         }
         double tp = 0.0;
         for (int64_t t = a + lane; t < b; t += G) tp += U[t] * x[t];
@@ -128,17 +132,22 @@ resid_rows_kernel(const mq_market mk, const double *__restrict__ x, double2 *__r
 #ifndef MQ_RP_LB
 #define MQ_RP_LB 2  // entries per lane batched ahead of the atomics
 #endif
+#ifndef MQ_RP_LONG_GRID
+#define MQ_RP_LONG_GRID 296  // CTAs of the long-row residual pass (grid + this <= MQ_MAX_BLOCKS)
+#endif
 #ifndef MQ_RP_GRID
 #define MQ_RP_GRID 444  // CTAs of the residual row passes: 3 per SM on 148 SMs; fixes the
                         // order of the objective's block partials (C4 sweep, DESIGN.md §11:
                         // 2/4/1024 -> 12.7 ms, 3/2/444 -> 10.2 ms per check)
 #endif
+static_assert(MQ_RP_GRID + MQ_RP_LONG_GRID <= MQ_MAX_BLOCKS, "partial slots");
 template <int G>
 __global__ void __launch_bounds__(256, MQ_RP_MINB)
 resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
                   const uint8_t *__restrict__ xflag, const double *__restrict__ xbar,
                   const double *__restrict__ xsum, const int64_t *__restrict__ navg,
-                  double4 *__restrict__ pc4, double *__restrict__ sa, double *__restrict__ sb) {
+                  double4 *__restrict__ pc4, double *__restrict__ sa, double *__restrict__ sb,
+                  int skip_long) {
     const double *__restrict__ U = mk.u_orig;
     // xsum != NULL: the average is read as xsum / navg, bit for bit what
     // avg_materialize_kernel would store (one reciprocal, one product)
@@ -157,11 +166,15 @@ resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
     double *misc[2] = {sa + kMisc, sb + kMisc};
     for (int64_t base = warp_id * RPW; base < mk.n; base += nwarps * RPW) {
         const int64_t i = base + gsub;
-        const bool has = i < mk.n;
+        bool has = i < mk.n;
         int64_t a = 0, b = 0;
         if (has) {
             a = mk.row_ptr[i];
             b = mk.row_ptr[i + 1];
+        }
+        if (has && skip_long && b - a > MQ_LONG_ROW) {  // resid_pair_long_kernel's row
+            has = false;  // the group still joins its warp's shuffles
+            b = a;
         }
         double tp = 0.0, tq = 0.0;
         for (int64_t t = a + lane; t < b; t += G) {
@@ -259,6 +272,207 @@ resid_pair_kernel(const mq_market mk, const double *__restrict__ x,
         if (threadIdx.x == 0) {
             sc[kSlotObj * MQ_MAX_BLOCKS + blockIdx.x] = ob;
             sc[kSlotBad * MQ_MAX_BLOCKS + blockIdx.x] = nb;
+        }
+    }
+}
+
+// resid_rows_kernel's rows longer than MQ_LONG_ROW, one CTA per row with
+// resid_pair_long_kernel's assignment and entry-to-thread map (so the two
+// passes stay bitwise the fused one).
+template <int T>
+__global__ void __launch_bounds__(T)
+resid_rows_long_kernel(const mq_market mk, const double *__restrict__ x,
+                       double2 *__restrict__ pc, int use_norm, double *__restrict__ t_out,
+                       double *__restrict__ y_out, double *__restrict__ scratch, int slot0) {
+    const double *__restrict__ U = use_norm ? mk.u : mk.u_orig;
+    const int tid = threadIdx.x;
+    __shared__ double sm[32];
+    __shared__ double tb;
+    double *misc = scratch + kMisc;
+    double ymax = 0.0, gmax = 0.0, xmax = 0.0, emax = 0.0, obj = 0.0, nbad = 0.0;
+    for (int64_t r = blockIdx.x; r < mk.nlong; r += gridDim.x) {
+        const int64_t i = mk.long_rows[r];
+        MQ_CHECK(i >= 0 && i < mk.n);
+        const int64_t a = mk.row_ptr[i], b = mk.row_ptr[i + 1];
+        double tp = 0.0;
+        for (int64_t t = a + tid; t < b; t += T) tp += U[t] * x[t];
+        tp = block_sum(tp, sm);
+        if (tid == 0) tb = tp;
+        __syncthreads();
+        const double t_i = tb;
+        __syncthreads();
+        const bool ok = t_i > 0.0;
+        if (!ok) {
+            if (tid == 0) {
+                nbad += 1.0;
+                atomicMin((unsigned long long *)(misc + 4),
+                          (unsigned long long)(mk.row_begin + i));
+                if (t_out) t_out[i] = t_i;
+                if (y_out) y_out[i] = 0.0;
+            }
+            continue;  // block-uniform
+        }
+        const double y = mk.w[i] / t_i;
+        if (tid == 0) {
+            obj += mk.w[i] * log(t_i);
+            ymax = fmax(ymax, y);
+            if (t_out) t_out[i] = t_i;
+            if (y_out) y_out[i] = y;
+        }
+        for (int64_t t = a + tid; t < b; t += T) {
+            const int32_t j = mk.col[t];
+            const double uy = U[t] * y;
+            const double2 pcj = __ldcg(pc + j);
+            if (uy > pcj.y) atomic_max_nonneg(reinterpret_cast<double *>(pc + j) + 1, uy);
+            const double es = fmax(pcj.x - uy, 0.0);
+            const double xv = x[t];
+            gmax = fmax(gmax, xv * es);
+            xmax = fmax(xmax, fabs(xv));
+            emax = fmax(emax, es);
+        }
+    }
+    ymax = group_max<32>(ymax);
+    gmax = group_max<32>(gmax);
+    xmax = group_max<32>(xmax);
+    emax = group_max<32>(emax);
+    if ((tid & 31) == 0) {
+        atomic_max_nonneg(misc + 0, ymax);
+        atomic_max_nonneg(misc + 1, gmax);
+        atomic_max_nonneg(misc + 2, xmax);
+        atomic_max_nonneg(misc + 3, emax);
+    }
+    const double ob = block_sum(obj, sm);
+    const double nb = block_sum(nbad, sm);
+    if (tid == 0) {
+        scratch[kSlotObj * MQ_MAX_BLOCKS + slot0 + blockIdx.x] = ob;
+        scratch[kSlotBad * MQ_MAX_BLOCKS + slot0 + blockIdx.x] = nb;
+    }
+}
+
+// The rows longer than MQ_LONG_ROW (mk.long_rows, longest first) of the
+// residual pair, one CTA per row (static cyclic assignment: the partial
+// sums' order depends only on the market): on power-law markets a
+// G-lane group would leave the few longest rows as the pass's tail.  The
+// same per-entry work as resid_pair_kernel; each CTA's objective and
+// bad-row partials go to partial slot slot0 + blockIdx.x.
+template <int T>
+__global__ void __launch_bounds__(T)
+resid_pair_long_kernel(const mq_market mk, const double *__restrict__ x,
+                       const uint8_t *__restrict__ xflag, const double *__restrict__ xbar,
+                       const double *__restrict__ xsum, const int64_t *__restrict__ navg,
+                       double4 *__restrict__ pc4, double *__restrict__ sa,
+                       double *__restrict__ sb, int slot0) {
+    const double *__restrict__ U = mk.u_orig;
+    const double cnt = xsum ? (double)*navg : 0.0;
+    const bool lazy = cnt > 0.0;
+    const double inv = lazy ? 1.0 / cnt : 0.0;
+    const double *__restrict__ xb = lazy ? xsum : xbar;
+    const double sc = lazy ? inv : 1.0;
+    const int tid = threadIdx.x;
+    __shared__ double sm[32];
+    __shared__ double tb[2];
+    double ym[2] = {0.0, 0.0}, gm[2] = {0.0, 0.0}, xm[2] = {0.0, 0.0}, em[2] = {0.0, 0.0};
+    double obj[2] = {0.0, 0.0}, nbad[2] = {0.0, 0.0};
+    double *misc[2] = {sa + kMisc, sb + kMisc};
+    for (int64_t r = blockIdx.x; r < mk.nlong; r += gridDim.x) {
+        const int64_t i = mk.long_rows[r];
+        MQ_CHECK(i >= 0 && i < mk.n);
+        const int64_t a = mk.row_ptr[i], b = mk.row_ptr[i + 1];
+        double tp = 0.0, tq = 0.0;
+        for (int64_t t = a + tid; t < b; t += T) {
+            const double ut = U[t];
+            if (xflag[t]) tp += ut * x[t];
+            tq += ut * (xb[t] * sc);
+        }
+        tp = block_sum(tp, sm);
+        tq = block_sum(tq, sm);
+        if (tid == 0) {
+            tb[0] = tp;
+            tb[1] = tq;
+        }
+        __syncthreads();
+        const double ti[2] = {tb[0], tb[1]};
+        __syncthreads();  // tb is rewritten by the next row
+        bool ok[2];
+        double y[2] = {0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            ok[k] = ti[k] > 0.0;
+            if (!ok[k] && tid == 0) {
+                nbad[k] += 1.0;
+                atomicMin((unsigned long long *)(misc[k] + 4),
+                          (unsigned long long)(mk.row_begin + i));
+            }
+            if (ok[k]) {
+                y[k] = mk.w[i] / ti[k];
+                if (tid == 0) {
+                    obj[k] += mk.w[i] * log(ti[k]);
+                    ym[k] = fmax(ym[k], y[k]);
+                }
+            }
+        }
+        if (!ok[0] && !ok[1]) continue;  // block-uniform
+        constexpr int LB = MQ_RP_LB;
+        for (int64_t t0 = a + tid; t0 < b; t0 += LB * T) {
+            int32_t jv[LB];
+            double uv[LB], xv[LB], bv[LB];
+            double2 q01[LB], q23[LB];
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                const int64_t t = t0 + q * T;
+                const bool in = t < b;
+                jv[q] = in ? mk.col[t] : 0;
+                MQ_CHECK(jv[q] >= 0 && jv[q] < mk.m);
+                uv[q] = in ? U[t] : 0.0;
+                xv[q] = (in && xflag[t]) ? x[t] : 0.0;
+                bv[q] = in ? xb[t] * sc : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < LB; ++q)
+                asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+                             : "=d"(q01[q].x), "=d"(q01[q].y), "=d"(q23[q].x), "=d"(q23[q].y)
+                             : "l"(pc4 + jv[q]));
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                if (t0 + q * T >= b) continue;
+                const int32_t j = jv[q];
+                if (ok[0]) {
+                    const double uy = uv[q] * y[0];
+                    if (uy > q01[q].y)
+                        atomic_max_nonneg(reinterpret_cast<double *>(pc4 + j) + 1, uy);
+                    const double es = fmax(q01[q].x - uy, 0.0);
+                    gm[0] = fmax(gm[0], xv[q] * es);
+                    xm[0] = fmax(xm[0], fabs(xv[q]));
+                    em[0] = fmax(em[0], es);
+                }
+                if (ok[1]) {
+                    const double uy = uv[q] * y[1];
+                    if (uy > q23[q].y)
+                        atomic_max_nonneg(reinterpret_cast<double *>(pc4 + j) + 3, uy);
+                    const double es = fmax(q23[q].x - uy, 0.0);
+                    gm[1] = fmax(gm[1], bv[q] * es);
+                    xm[1] = fmax(xm[1], fabs(bv[q]));
+                    em[1] = fmax(em[1], es);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const double a0 = group_max<32>(ym[k]), a1 = group_max<32>(gm[k]);
+        const double a2 = group_max<32>(xm[k]), a3 = group_max<32>(em[k]);
+        if ((tid & 31) == 0) {
+            atomic_max_nonneg(misc[k] + 0, a0);
+            atomic_max_nonneg(misc[k] + 1, a1);
+            atomic_max_nonneg(misc[k] + 2, a2);
+            atomic_max_nonneg(misc[k] + 3, a3);
+        }
+        const double ob = block_sum(obj[k], sm);
+        const double nb = block_sum(nbad[k], sm);
+        double *scr = k ? sb : sa;
+        if (tid == 0) {
+            scr[kSlotObj * MQ_MAX_BLOCKS + slot0 + blockIdx.x] = ob;
+            scr[kSlotBad * MQ_MAX_BLOCKS + slot0 + blockIdx.x] = nb;
         }
     }
 }
@@ -439,10 +653,16 @@ int mq_resid_rows(const mq_market *mk, const double *x, const double *p, int use
     }
     const int gm = grid_for(mk->m, 256, MQ_MAX_BLOCKS);
     pc_init_kernel<<<gm, 256, 0, s>>>(mk->m, p, pc);
-    resid_rows_kernel<8><<<grid, 256, 0, s>>>(*mk, x, pc, use_norm, t_out, y_out, scratch);
+    const int glong = mk->nlong > 0 && mk->long_rows
+                          ? grid_for(mk->nlong, 1, MQ_RP_LONG_GRID) : 0;
+    resid_rows_kernel<8><<<grid, 256, 0, s>>>(*mk, x, pc, use_norm, t_out, y_out, scratch,
+                                              glong > 0);
+    if (glong)
+        resid_rows_long_kernel<256><<<glong, 256, 0, s>>>(*mk, x, pc, use_norm, t_out, y_out,
+                                                          scratch, grid);
     pc_out_kernel<<<gm, 256, 0, s>>>(mk->m, pc, colbest);
     if (!work) cudaFreeAsync(pc, s);
-    sum_slots_kernel<<<1, 64, 0, s>>>(scratch, grid, 2, scratch + kMisc + 16);
+    sum_slots_kernel<<<1, 64, 0, s>>>(scratch, grid + glong, 2, scratch + kMisc + 16);
     resid_rows_finish<<<1, 1, 0, s>>>(scratch, scratch + kMisc + 16, row_out);
     return check_launch("mq_resid_rows");
 }
@@ -461,14 +681,20 @@ int mq_resid_rows_pair(const mq_market *mk, const mq_state *st, double *colbest_
     double4 *pc4 = reinterpret_cast<double4 *>(work);
     const int gm = grid_for(mk->m, 256, MQ_MAX_BLOCKS);
     pc4_init_kernel<<<gm, 256, 0, s>>>(mk->m, st->p, st->pbar, pc4);
-    resid_pair_kernel<8><<<grid, 256, 0, s>>>(*mk, st->x, st->xflag, st->xbar,
-                                              st->xbar_lazy ? st->xsum : nullptr, st->navg,
-                                              pc4, scratch_last,
-                                              scratch_avg);
+    const double *xs = st->xbar_lazy ? st->xsum : nullptr;
+    // long rows (if any) get a CTA each; their partials follow the main grid's
+    const int glong = mk->nlong > 0 && mk->long_rows
+                          ? grid_for(mk->nlong, 1, MQ_RP_LONG_GRID) : 0;
+    resid_pair_kernel<8><<<grid, 256, 0, s>>>(*mk, st->x, st->xflag, st->xbar, xs, st->navg,
+                                              pc4, scratch_last, scratch_avg, glong > 0);
+    if (glong)
+        resid_pair_long_kernel<256><<<glong, 256, 0, s>>>(*mk, st->x, st->xflag, st->xbar, xs,
+                                                          st->navg, pc4, scratch_last,
+                                                          scratch_avg, grid);
     pc4_out_kernel<<<gm, 256, 0, s>>>(mk->m, pc4, colbest_last, colbest_avg);
-    sum_slots_kernel<<<1, 64, 0, s>>>(scratch_last, grid, 2, scratch_last + kMisc + 16);
+    sum_slots_kernel<<<1, 64, 0, s>>>(scratch_last, grid + glong, 2, scratch_last + kMisc + 16);
     resid_rows_finish<<<1, 1, 0, s>>>(scratch_last, scratch_last + kMisc + 16, row_out_last);
-    sum_slots_kernel<<<1, 64, 0, s>>>(scratch_avg, grid, 2, scratch_avg + kMisc + 16);
+    sum_slots_kernel<<<1, 64, 0, s>>>(scratch_avg, grid + glong, 2, scratch_avg + kMisc + 16);
     resid_rows_finish<<<1, 1, 0, s>>>(scratch_avg, scratch_avg + kMisc + 16, row_out_avg);
     return check_launch("mq_resid_rows_pair");
 }

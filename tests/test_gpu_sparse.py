@@ -97,7 +97,8 @@ def test_restart_resets_the_running_sum():
 def test_fused_residual_pair_is_bitwise_the_two_passes():
     """mq_resid_rows_pair (one sweep for the last and the averaged iterate)
     against the two separate mq_resid_rows passes, mid-solve on a generated
-    market with medium rows: identical residuals and column maxima.  The
+    market with medium and long rows (the latter a CTA each in both):
+    identical residuals and column maxima.  The
     fused sweep runs before x̄ is formed (it reads xsum / navg), the separate
     passes after: the lazy average is bit for bit the formed one."""
     import torch
