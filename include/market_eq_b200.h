@@ -32,13 +32,15 @@
 extern "C" {
 #endif
 
-#define MQ_ABI_VERSION 10
+#define MQ_ABI_VERSION 11
 #define MQ_TILE_ENTRIES 2560 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
 #define MQ_REG_ROW 128        /* tile rows longer than this (medium rows) are
                                  solved by the warp-per-row path          */
-#define MQ_WS_SLOTS 12        /* working-set slots per row (screened solve)  */
+#ifndef MQ_WS_SLOTS
+#define MQ_WS_SLOTS 10        /* working-set slots per row (screened solve)  */
+#endif
 #define MQ_WS_MAX_ROW 256     /* rows up to this length have working sets    */
 
 /* Read-only market description (device pointers, borrowed).  Arrays marked
@@ -180,6 +182,10 @@ typedef struct mq_state {
                            mq_avg_xbar after the last chunk);
                            mq_resid_rows_pair reads the average as
                            xsum / navg instead                               */
+    uint8_t *ws_lvl;    /* [n] per row: the working-set width level (gamma =
+                           1.001, 1.005, 1.02, 1.06 for 0..3; +1 after a
+                           failed certificate, -1 after an overfull set or
+                           a rebuild of all sets); NULL: level 2             */
 } mq_state;
 
 /* Mutable iterate of the lifted PDHG path (algo="pdhg", kernels.py:146-197):

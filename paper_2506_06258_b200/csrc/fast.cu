@@ -411,7 +411,7 @@ __device__ __forceinline__ double row_root_warm(const double (&c)[PER], const do
 // enter the root (masked) nor change.  A row whose zero entries satisfy that
 // with margin at the row's root can therefore be solved over the rest —
 // its working set: the nonzero entries plus the zero entries within a factor
-// MQ_WS_GAMMA of the threshold — and gives exactly the full row's active set,
+// gamma of the threshold — and gives exactly the full row's active set,
 // root and allocation.  The certificate needs no look at the screened
 // entries: their prices have dropped by at most D (drift) since the working
 // set was built, so p_j s >= (p_j^ref - D) s >= theta (1 - D / P) s with
@@ -419,9 +419,32 @@ __device__ __forceinline__ double row_root_warm(const double (&c)[PER], const do
 // hold ~5 % of the entries and the certificate holds for ~100 % of the rows
 // (tools/screen_stats.py, tools/ws_stats.py): one price gather in ~20 instead
 // of every entry's.
-#ifndef MQ_WS_GAMMA
-#define MQ_WS_GAMMA 1.03
+// The factor is per row (mq_state.ws_lvl): a row whose certificate failed
+// is rebuilt one level wider, a row with more working entries than slots one
+// level narrower, and every row one level narrower when all working sets
+// are rebuilt (after a restart).  Narrow sets are cheap; rows whose prices
+// move fast widen theirs instead of failing every few iterations.
+#ifndef MQ_WS_G0
+#define MQ_WS_G0 1.001
 #endif
+#ifndef MQ_WS_G1
+#define MQ_WS_G1 1.005
+#endif
+#ifndef MQ_WS_G2
+#define MQ_WS_G2 1.02
+#endif
+#ifndef MQ_WS_G3
+#define MQ_WS_G3 1.06
+#endif
+#ifndef MQ_WS_POOL_GAMMA
+#define MQ_WS_POOL_GAMMA 1.03  // the medium / long rows' pools
+#endif
+__device__ __forceinline__ double ws_gamma(int lvl) {
+    return lvl <= 0 ? MQ_WS_G0 : lvl == 1 ? MQ_WS_G1 : lvl == 2 ? MQ_WS_G2 : MQ_WS_G3;
+}
+__device__ __forceinline__ int ws_level(const mq_state &st, int64_t i) {
+    return st.ws_lvl ? (int)st.ws_lvl[i] : 2;
+}
 #ifndef MQ_WS_MARGIN
 #define MQ_WS_MARGIN 1e-12
 #endif
@@ -464,9 +487,10 @@ template <int G, int RP>
 __device__ __forceinline__ void ws_build(const mq_state &st, int64_t i, int lane, int gsub,
                                          bool build, int len, double w, double s, double cnow,
                                          const double (&u)[RP], const double (&pv)[RP],
-                                         const double (&xn)[RP], const int (&jc)[RP]) {
+                                         const double (&xn)[RP], const int (&jc)[RP],
+                                         double gamma) {
     constexpr int K = MQ_WS_SLOTS;
-    const double gw = MQ_WS_GAMMA * w;
+    const double gw = gamma * w;
     int before = 0, rank[RP];
     uint32_t hot = 0;
     // smallest p / u over the screened entries: the pair is picked by
@@ -734,9 +758,15 @@ primal_fused_kernel(const mq_market mk, const mq_state st, int it, double *__res
                     jc[e] = t < b ? scol[t] : 0;
                     if (t < b) put_x(mk, st, e0 + t, jc[e], xn[e], (fb >> e) & 1u);
                 }
-                if (BUILD)  // the working sets of every row, rebuilt at once
+                if (BUILD) {  // the working sets of every row, rebuilt at once, one level narrower
+                    int lvl = has ? ws_level(st, r0 + r) : 0;
+                    if (lvl > 0) {
+                        --lvl;
+                        if (lane == 0 && st.ws_lvl) st.ws_lvl[r0 + r] = (uint8_t)lvl;
+                    }
                     ws_build<G, RP>(st, r0 + r, lane, gsub, has, b - a, has ? sw[r] : 0.0, sr,
-                                    drift_now(st), u, pv, xn, jc);
+                                    drift_now(st), u, pv, xn, jc, ws_gamma(lvl));
+                }
                 MQ_TS(tq3);
                 MQ_TA(5, tq0, tq1);
                 MQ_TA(6, tq1, tq2);
@@ -1123,7 +1153,7 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
             // T entries so the block scan ranks working entries in ascending
             // position: nonzero entries and zero entries near the threshold
             const int64_t po = r * (int64_t)CAP;
-            const double gw = MQ_WS_GAMMA * wi;
+            const double gw = MQ_WS_POOL_GAMMA * wi;
             const int lane = tid & 31, warp = tid >> 5;
             int base = 0;
             double bp = CUDART_INF, bu = 1.0, pmn = CUDART_INF;
@@ -1348,7 +1378,7 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
             // write-back fused with the pool rebuild: warp-wide chunks of 32
             // entries in ascending position, ballots rank the working entries
             // (nonzero, or zero with p_j s < gamma w u_j)
-            const double gw = MQ_WS_GAMMA * wi;
+            const double gw = MQ_WS_POOL_GAMMA * wi;
             int base = 0;
             double bp = CUDART_INF, bu = 1.0, pmn = CUDART_INF;
             for (int b0 = 0; b0 < len; b0 += LB * G) {  // warp-uniform bounds
@@ -1853,7 +1883,12 @@ ws_full_kernel(const mq_market mk, const mq_state st, int it, double *__restrict
                 }
             }
         }
-        ws_build<G, RP>(st, i, lane, gsub, has && hold != -3, len, w, s, cnow, u, pv, xn, jc);
+        // a failed certificate widens the row's set, an overfull one narrows it
+        int lvl = has ? ws_level(st, i) : 0;
+        const int nl = hold >= 0 ? (lvl < 3 ? lvl + 1 : 3) : hold == -2 ? (lvl > 0 ? lvl - 1 : 0) : lvl;
+        if (has && hold != -3 && nl != lvl && lane == 0 && st.ws_lvl) st.ws_lvl[i] = (uint8_t)nl;
+        ws_build<G, RP>(st, i, lane, gsub, has && hold != -3, len, w, s, cnow, u, pv, xn, jc,
+                        ws_gamma(nl));
         if (has && lane == 0) {
             st.srow[i] = s;
             my_sweeps += nsw;

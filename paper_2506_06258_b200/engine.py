@@ -273,7 +273,7 @@ class PdhcgEngine:
         self.working_set = bool(working_set and self.sparse and hasattr(dm, "lib")
                                 and not colsum_fp64)
         if self.working_set:
-            K = nat.WS_SLOTS
+            K = int(dm.lib.mq_ws_slots())  # nat.WS_SLOTS in the shipped build
             lens = dm.row_ptr[1:] - dm.row_ptr[:-1]
             self.ws_init = torch.where(lens > nat.WS_MAX_ROW, -3, -1).to(torch.int32)
             if dm.long_rows.numel():
@@ -316,6 +316,8 @@ class PdhcgEngine:
                 self.pm_col = torch.zeros(nml * C, dtype=torch.int32, device=dev)
                 self.pm_pos = torch.zeros(nml * C, dtype=torch.int32, device=dev)
             self.drift = torch.zeros(2, **f64)
+            # per-row working-set width level (kept across invalidations)
+            self.ws_lvl = torch.zeros(max(1, dm.n), dtype=torch.uint8, device=dev)
         # fixed-point column sums: m u64 accumulators, zero between iterations
         fixed = getattr(getattr(dm, "lib", None), "mq_fixed_colsum", None)
         self.fixed = bool(fixed is not None and fixed() == 1 and self.mode != "ksection")
@@ -375,7 +377,7 @@ class PdhcgEngine:
             setattr(s, name, getattr(self, name).data_ptr())
         if self.working_set:
             for name in ("ws_hdr", "ws_kmax", "ws_u", "ws_x", "ws_col", "ws_pos", "ws_list",
-                         "drift"):
+                         "drift", "ws_lvl"):
                 setattr(s, name, getattr(self, name).data_ptr())
             if self.pool:
                 for name in ("pl_hdr", "pl_u", "pl_x", "pl_col", "pl_pos"):

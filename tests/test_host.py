@@ -24,7 +24,7 @@ def test_native_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(lib, name)
-    assert lib.mq_abi_version() == 10
+    assert lib.mq_abi_version() == 11
     assert lib.mq_med_cap() == _native.MED_CAP and lib.mq_long_cap() == _native.LONG_CAP
     assert lib.mq_scratch_doubles() > 0
 
