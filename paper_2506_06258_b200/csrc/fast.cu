@@ -1492,13 +1492,8 @@ struct WsStage {
     uint8_t pos[SB * K * 32];
 };
 using WsStageT = WsStage<MQ_WS_SLOTS, MQ_WS_SB>;
-#ifdef MQ_WS_CPASYNC
-constexpr int kWsGatherSmem = MQ_WS_NC * MQ_WS_SLOTS * 32 * 8;  // per-consumer gather slots
-#else
-constexpr int kWsGatherSmem = 0;
-#endif
 constexpr int kWsSmem =
-    MQ_WS_NST * (int)sizeof(WsStageT) + MQ_WS_NST * (2 * 8 + 8 + 4) + 64 + kWsGatherSmem;
+    MQ_WS_NST * (int)sizeof(WsStageT) + MQ_WS_NST * (2 * 8 + 8 + 4) + 64;
 static_assert(sizeof(WsStageT) % 16 == 0, "stage must keep 16-byte alignment");
 
 __global__ void __launch_bounds__((MQ_WS_NC + 1) * 32, 1)
@@ -1627,12 +1622,6 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
         MQ_CHECK(h >= -3 && h <= K);
         if (force_full && h != -3) h = -1;
         uint32_t was = 0;  // slots whose x was nonzero
-#ifdef MQ_WS_CPASYNC
-        // the price gathers land in the warp's own shared-memory slots
-        // (cp.async): no registers held while they are in flight
-        double *pg = reinterpret_cast<double *>(wsm + NST * sizeof(WsStageT) + NST * (2 * 8 + 8 + 4) + 64) +
-                     warp * K * 32;
-#endif
 #pragma unroll
         for (int k = 0; k < K; ++k) {  // the price gathers leave before the release
             u[k] = 0.0;
@@ -1642,14 +1631,7 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
                 u[k] = d.u[so + k * 32];
                 c[k] = d.x[so + k * 32];
                 MQ_CHECK(d.col[so + k * 32] >= 0 && d.col[so + k * 32] < mk.m);
-#ifdef MQ_WS_CPASYNC
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                                 smem_addr(pg + k * 32 + lane)),
-                             "l"(st.p + d.col[so + k * 32])
-                             : "memory");
-#else
                 pv[k] = __ldg(st.p + d.col[so + k * 32]);
-#endif
                 if (c[k] > 0.0) was |= 1u << k;
             }
         }
@@ -1658,15 +1640,8 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
         if (!mine) continue;
         ws_push(st, h == -1 || h == -2, i);
         const bool act = h >= 0;
-#ifdef MQ_WS_CPASYNC
-        asm volatile("cp.async.wait_all;" ::: "memory");
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-            if (k < h) c[k] -= tau * pg[k * 32 + lane];
-#else
 #pragma unroll
         for (int k = 0; k < K; ++k) c[k] -= tau * pv[k];
-#endif
         const double tw = tau * w;
         // ---- exact root over the working set (row_root_warm, one thread)
         auto amask = [&](double z) -> uint32_t {
