@@ -132,6 +132,9 @@ resid_rows_kernel(const mq_market mk, const double *__restrict__ x, double2 *__r
 #ifndef MQ_RP_LB
 #define MQ_RP_LB 2  // entries per lane batched ahead of the atomics
 #endif
+#ifndef MQ_RP_G
+#define MQ_RP_G 8  // lanes per row of the residual row passes (32 / MQ_RP_G rows per warp)
+#endif
 #ifndef MQ_RP_LONG_GRID
 #define MQ_RP_LONG_GRID 296  // CTAs of the long-row residual pass (grid + this <= MQ_MAX_BLOCKS)
 #endif
@@ -655,7 +658,7 @@ int mq_resid_rows(const mq_market *mk, const double *x, const double *p, int use
     pc_init_kernel<<<gm, 256, 0, s>>>(mk->m, p, pc);
     const int glong = mk->nlong > 0 && mk->long_rows
                           ? grid_for(mk->nlong, 1, MQ_RP_LONG_GRID) : 0;
-    resid_rows_kernel<8><<<grid, 256, 0, s>>>(*mk, x, pc, use_norm, t_out, y_out, scratch,
+    resid_rows_kernel<MQ_RP_G><<<grid, 256, 0, s>>>(*mk, x, pc, use_norm, t_out, y_out, scratch,
                                               glong > 0);
     if (glong)
         resid_rows_long_kernel<256><<<glong, 256, 0, s>>>(*mk, x, pc, use_norm, t_out, y_out,
@@ -685,7 +688,7 @@ int mq_resid_rows_pair(const mq_market *mk, const mq_state *st, double *colbest_
     // long rows (if any) get a CTA each; their partials follow the main grid's
     const int glong = mk->nlong > 0 && mk->long_rows
                           ? grid_for(mk->nlong, 1, MQ_RP_LONG_GRID) : 0;
-    resid_pair_kernel<8><<<grid, 256, 0, s>>>(*mk, st->x, st->xflag, st->xbar, xs, st->navg,
+    resid_pair_kernel<MQ_RP_G><<<grid, 256, 0, s>>>(*mk, st->x, st->xflag, st->xbar, xs, st->navg,
                                               pc4, scratch_last, scratch_avg, glong > 0);
     if (glong)
         resid_pair_long_kernel<256><<<glong, 256, 0, s>>>(*mk, st->x, st->xflag, st->xbar, xs,
