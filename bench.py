@@ -52,18 +52,57 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: an NVML
+    polling thread (every ~0.5 ms, so even a 20 ms region gets dozens of
+    samples); nvidia-smi -lms 200 if NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.lines = []
+        self.samples = []  # (t, sm_mhz, reason bits) from NVML
+        self.nvml = None
+        self.stop = threading.Event()
+
+    def _handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        try:  # the CUDA device's own GPU, whatever CUDA_VISIBLE_DEVICES maps
+            uuid = str(torch.cuda.get_device_properties(self.index).uuid)
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID(
+                uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self, nv, h):
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((time.perf_counter(), float(sm), int(rs)))
+            except Exception:
+                pass
+            time.sleep(0.0005)
 
     def __enter__(self):
+        try:
+            nv, h = self._handle()
+            self.nvml = (nv, h, float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
+            self.t = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self.t.start()
+            while not self.samples and self.t.is_alive():  # polling before the region starts
+                time.sleep(0.0002)
+            self.t0 = time.perf_counter()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -80,6 +119,10 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self.t1 = time.perf_counter()
+            self.stop.set()
+            self.t.join(timeout=5)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -88,8 +131,23 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if self.nvml is not None:
+            nv, _, mx = self.nvml
+            inside = [x for x in self.samples if self.t0 <= x[0] <= self.t1]
+            if not inside and self.samples:  # region shorter than a poll: the nearest ones
+                inside = sorted(self.samples, key=lambda x: min(abs(x[0] - self.t0),
+                                                                abs(x[0] - self.t1)))[:2]
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            reasons = sorted({k for _, _, r in inside for k, b in bits.items() if r & b})
+            if not inside:
+                return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0,
+                        "source": "nvml"}
+            return {"sm_mhz": statistics.median(x[1] for x in inside), "sm_max_mhz": mx,
+                    "reasons": reasons, "samples": len(inside), "source": "nvml"}
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
@@ -99,13 +157,13 @@ class ClockSampler:
                 mx.append(float(parts[1]))
             except ValueError:
                 continue
-            for name, v in zip(names, parts[2:6]):
+            for name, v in zip(self.NAMES, parts[2:6]):
                 if v.lower() == "active":
                     reasons.add(name)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
 # ------------------------------------------------------------------ workload
@@ -164,6 +222,19 @@ def make_session(shard, group):
     eng.set_steps(ctrl.tau, ctrl.sigma)
     torch.cuda.synchronize()
     return dm, eng
+
+
+def warm_graphs(eng, iters, chunk=40):
+    """Capture (not run) the chunk graphs run_iters(eng, iters) will replay,
+    so no capture falls inside a timed region."""
+    if not getattr(eng, "use_graphs", False):
+        return
+    for c in {min(chunk, iters)} | ({iters % chunk} if iters > chunk and iters % chunk else set()):
+        if (c, False) not in eng._graphs:
+            try:
+                eng._capture(c, False)
+            except Exception:  # capture unsupported here: run_chunk falls back itself
+                return
 
 
 def run_iters(eng, iters, chunk=40):
@@ -355,6 +426,7 @@ def main():
                                                device="cuda")).item())
 
     run_iters(eng, a.warmup)
+    warm_graphs(eng, a.steps)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
