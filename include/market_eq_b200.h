@@ -387,6 +387,9 @@ int mq_ws_slots(void);
 int mq_long_cap(void);
 /* MQ_MED_CAP: entries of a medium row's working-set pool (mq_state.pm_*) */
 int mq_med_cap(void);
+/* sizeof(mq_market), sizeof(mq_state) of this build (binding layout checks) */
+int mq_market_bytes(void);
+int mq_state_bytes(void);
 /* 1 if the build keeps the sparse iterate (xflag / xsum) */
 int mq_x_sparse(void);
 /* sparse iterate, after mq_chunk_end: the screened rows' x and flags from

@@ -106,6 +106,8 @@ _SIGS = {
     "mq_ws_slots": (CINT, []),
     "mq_long_cap": (CINT, []),
     "mq_med_cap": (CINT, []),
+    "mq_market_bytes": (CINT, []),
+    "mq_state_bytes": (CINT, []),
     "mq_avg_materialize": (CINT, [PM, PS, P]),
     "mq_ws_flush": (CINT, [PM, PS, P]),
     "mq_avg_xbar": (CINT, [PM, PS, P]),

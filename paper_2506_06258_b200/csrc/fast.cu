@@ -2157,6 +2157,8 @@ int mq_fixed_colsum(void) { return 1; }
 int mq_ws_slots(void) { return MQ_WS_SLOTS; }
 int mq_long_cap(void) { return MQ_LONG_CAP; }
 int mq_med_cap(void) { return MQ_MED_CAP; }
+int mq_market_bytes(void) { return (int)sizeof(mq_market); }
+int mq_state_bytes(void) { return (int)sizeof(mq_state); }
 
 int mq_colsum(const mq_market *mk, const double *v, double *out, void *stream) {
     const int grid = (int)((mk->m + 255) / 256);

@@ -25,6 +25,9 @@ def test_native_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(lib, name)
     assert lib.mq_abi_version() == 11
+    # the ctypes mirrors have the C layout
+    assert lib.mq_market_bytes() == ctypes.sizeof(_native.MqMarket)
+    assert lib.mq_state_bytes() == ctypes.sizeof(_native.MqState)
     assert lib.mq_med_cap() == _native.MED_CAP and lib.mq_long_cap() == _native.LONG_CAP
     assert lib.mq_scratch_doubles() > 0
 
