@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define MQ_ABI_VERSION 11
+#define MQ_ABI_VERSION 12
 #define MQ_TILE_ENTRIES 2560 /* entries staged per shared-memory tile (default build) */
 #define MQ_LONG_ROW 1024      /* rows longer than this use the CTA-per-row path */
 #define MQ_TILE_ROWS 256      /* rows per tile                                */
@@ -186,6 +186,9 @@ typedef struct mq_state {
                            1.001, 1.005, 1.02, 1.06 for 0..3; +1 after a
                            failed certificate, -1 after an overfull set or
                            a rebuild of all sets); NULL: level 2             */
+    int32_t *pl_list;   /* [nlong] long rows left for the CTA-per-row kernel
+                           after the warp-per-row screened pass (count in
+                           blk_done[7]); used when pl_hdr is set             */
 } mq_state;
 
 /* Mutable iterate of the lifted PDHG path (algo="pdhg", kernels.py:146-197):

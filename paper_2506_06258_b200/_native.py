@@ -18,7 +18,7 @@ LONG_ROW = int(os.environ.get("MQ_LONG_ROW", "1024"))  # MQ_LONG_ROW (tuning ove
 REG_ROW = 128         # MQ_REG_ROW
 TILE_ROWS = 256       # MQ_TILE_ROWS
 PAD = 16              # padding elements after nnz arrays read by TMA bulk copies
-ABI_VERSION = 11
+ABI_VERSION = 12
 WS_SLOTS = 10          # MQ_WS_SLOTS
 WS_MAX_ROW = 256       # MQ_WS_MAX_ROW
 LONG_CAP = 1536        # MQ_LONG_CAP (long-row working-set pool per row)
@@ -60,7 +60,7 @@ class MqState(ctypes.Structure):
                 ("pl_hdr", P), ("pl_u", P), ("pl_x", P), ("pl_col", P), ("pl_pos", P),
                 ("pm_hdr", P), ("pm_u", P), ("pm_x", P), ("pm_col", P), ("pm_pos", P),
                 ("ws_rebuild", ctypes.c_int32), ("xbar_lazy", ctypes.c_int32),
-                ("ws_lvl", P)]
+                ("ws_lvl", P), ("pl_list", P)]
 
 
 PM = ctypes.POINTER(MqMarket)

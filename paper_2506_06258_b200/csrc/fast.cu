@@ -78,6 +78,9 @@
 #ifndef MQ_MED_CAP
 #define MQ_MED_CAP 128  // working-set pool of a medium row > MQ_WS_MAX_ROW (4 per lane)
 #endif
+#ifndef MQ_LONG_WCAP
+#define MQ_LONG_WCAP 128  // long-row pools up to this size are solved by a warp (primal_long_ws_kernel)
+#endif
 #ifndef MQ_LONG_CAP
 #define MQ_LONG_CAP 1536  // entries of a long row kept in shared memory (32 KB, 4 CTAs/SM:
                           // the rest of the carveout stays L1 for the price gathers)
@@ -929,7 +932,8 @@ struct LongSmem {
 
 template <int T, int CAP>
 __global__ void __launch_bounds__(T, MQ_LONG_PER_SM)
-primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out) {
+primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__restrict__ x_prev_out,
+                   int listed) {
     using L = LongSmem<T, CAP>;
     extern __shared__ __align__(16) unsigned char lsm[];
     double *s_u = reinterpret_cast<double *>(lsm + L::kU);
@@ -951,8 +955,12 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
         __syncthreads();  // the previous row's shared-memory reads are done
         if (tid == 0) claimed = atomicAdd(st.blk_done + 1, 1);
         __syncthreads();
-        const int64_t r = claimed;
-        if (r >= mk.nlong) break;
+        // listed: only the rows primal_long_ws_kernel left (pool too large
+        // for a warp, missing, or its certificate failed)
+        const int64_t nrows = listed ? *(volatile int32_t *)(st.blk_done + 7) : mk.nlong;
+        if (claimed >= nrows) break;
+        const int64_t r = listed ? (int64_t)st.pl_list[claimed] : claimed;
+        MQ_CHECK(r >= 0 && r < mk.nlong);
         const int64_t i = mk.long_rows[r];
         MQ_CHECK(i >= 0 && i < mk.n);
         const int64_t a = mk.row_ptr[i];
@@ -968,7 +976,8 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
             const int4 hd = reinterpret_cast<const int4 *>(st.pl_hdr)[r];
             const int h = hd.x;
             MQ_CHECK(h >= -2 && h <= CAP);
-            if (h >= 0) {
+            // a pool the warp pass could hold already failed there
+            if (h >= 0 && !(listed && h <= MQ_LONG_WCAP)) {
                 const int64_t po = r * (int64_t)CAP;
                 double s0w = 0.0, Aw = 0.0, Bw = 0.0;
                 for (int k = tid; k < h; k += T) {
@@ -1248,6 +1257,83 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
     if (tid == 0 && tot) atomicAdd((unsigned long long *)(st.pass_out + it), (unsigned long long)tot);
     const int64_t fl = block_sum_i64((int64_t)my_faults, red);
     if (tid == 0 && fl) atomicAdd((unsigned long long *)st.faults, (unsigned long long)fl);
+}
+
+// Long rows' screened pass, a warp per row: a pool of up to MQ_LONG_WCAP
+// entries is solved in registers (MQ_LONG_WCAP / 32 per lane) with the
+// certificate of the short rows; every other row (no pool, a larger one, a
+// failed certificate) is listed for primal_long_kernel.  Most long rows
+// work over a few dozen entries: a whole CTA per row idles on them.
+static_assert(MQ_LONG_WCAP % 32 == 0 && MQ_LONG_WCAP <= MQ_LONG_CAP, "warp pool cap");
+__global__ void __launch_bounds__(256)
+primal_long_ws_kernel(const mq_market mk, const mq_state st, int it) {
+    constexpr int G = 32, PC = MQ_LONG_WCAP / 32;
+    const double tau = st.steps[0];
+    const int lane = threadIdx.x & 31;
+    const double cnow = drift_now(st);
+    int my_sweeps = 0;
+    for (;;) {
+        int r = 0;
+        if (lane == 0) r = atomicAdd(st.blk_done + 6, 1);
+        r = __shfl_sync(MQ_FULL, r, 0);
+        if (r >= mk.nlong) break;  // warp-uniform
+        const int64_t i = mk.long_rows[r];
+        MQ_CHECK(i >= 0 && i < mk.n);
+        const int64_t e0 = mk.row_ptr[i];
+        const int len = (int)(mk.row_ptr[i + 1] - e0);
+        const double wi = mk.w[i];
+        const double tw = tau * wi;
+        const int4 hd = reinterpret_cast<const int4 *>(st.pl_hdr)[r];
+        const int h = hd.x;
+        MQ_CHECK(h >= -2 && h <= MQ_LONG_CAP);
+        bool solved = false;
+        if (h > 0 && h <= MQ_LONG_WCAP) {  // warp-uniform
+            const int64_t po = r * (int64_t)MQ_LONG_CAP;
+            double c[PC], u[PC], xk[PC];
+            int jc[PC], ps[PC];
+#pragma unroll
+            for (int e = 0; e < PC; ++e) {
+                const int k = lane + e * G;
+                const bool in = k < h;
+                u[e] = in ? __ldcg(st.pl_u + po + k) : 0.0;
+                xk[e] = in ? __ldcg(st.pl_x + po + k) : 0.0;
+                jc[e] = in ? __ldcg(st.pl_col + po + k) : 0;
+                ps[e] = in ? __ldcg(st.pl_pos + po + k) : 0;
+                MQ_CHECK(!in || (jc[e] >= 0 && jc[e] < mk.m && ps[e] >= 0 && ps[e] < len));
+            }
+#pragma unroll
+            for (int e = 0; e < PC; ++e)
+                c[e] = xk[e] - tau * (lane + e * G < h ? __ldg(st.p + jc[e]) : 0.0);
+            int nsw = 0;
+            bool ok = true;
+            const double sw = row_root_warm<G, PC>(c, u, tw, st.srow[i], true, MQ_FULL, &nsw, &ok);
+            const double th = (double)__int_as_float(hd.y), pm = (double)__int_as_float(hd.z);
+            const double D = fmax(__dsub_ru(cnow, (double)__int_as_float(hd.w)), 0.0);
+            const double lhs = __dmul_rd(__dmul_rd(th, sw), __dsub_rd(pm, D));
+            const double rhs = __dmul_ru(__dmul_ru(wi, pm), 1.0 + MQ_WS_MARGIN);
+            if (ok && lhs >= rhs && pm > D) {  // warp-uniform
+                const double inv_s = 1.0 / sw;
+#pragma unroll
+                for (int e = 0; e < PC; ++e) {
+                    const int k = lane + e * G;
+                    if (k < h) {
+                        const double xn = fmax(c[e] + tw * u[e] * inv_s, 0.0);
+                        const bool was = xk[e] > 0.0;
+                        if (xn > 0.0 || was) st.pl_x[po + k] = xn;
+                        put_x(mk, st, e0 + ps[e], jc[e], xn, was);
+                    }
+                }
+                if (lane == 0) {
+                    st.srow[i] = sw;
+                    my_sweeps += nsw;
+                }
+                solved = true;
+            }
+        }
+        if (!solved && lane == 0) st.pl_list[atomicAdd(st.blk_done + 7, 1)] = r;
+    }
+    if (lane == 0 && my_sweeps)
+        atomicAdd((unsigned long long *)(st.pass_out + it), (unsigned long long)my_sweeps);
 }
 
 // Medium rows (MQ_REG_ROW < length <= MQ_LONG_ROW, listed longest first in
@@ -2022,7 +2108,7 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
     int rc = 0;
     // every dynamic work counter (tiles, long rows, medium rows, full-solve
     // list and its claims, screened batches) restarts at 0
-    cudaMemsetAsync(st->blk_done, 0, 6 * sizeof(int32_t), s);
+    cudaMemsetAsync(st->blk_done, 0, 8 * sizeof(int32_t), s);
     if (st->ws_hdr && !st->ws_rebuild) {  // screened solve, then the full-solve list
         static unsigned long long wconfigured = 0;
         if (int rc2 = ensure_smem(ws_kernel, kWsSmem, &wconfigured,
@@ -2045,7 +2131,11 @@ int primal_launch(const mq_market *mk, const mq_state *st, int it, double *xprev
             return rc2;
         const int per_sm = MQ_LONG_PER_SM;
         const int grid = grid_for(mk->nlong, 1, sm_count() * per_sm);
-        lk<<<grid, MQ_LONG_THREADS, LS::kBytes, s>>>(*mk, *st, it, xprev);
+        // with pools: the warp pass first, the CTA kernel on the rows it left
+        const int listed = st->pl_hdr && st->pl_list && !xprev;
+        if (listed)
+            primal_long_ws_kernel<<<grid_for(mk->nlong, 8, sm_count() * 8), 256, 0, s>>>(*mk, *st, it);
+        lk<<<grid, MQ_LONG_THREADS, LS::kBytes, s>>>(*mk, *st, it, xprev, listed);
     }
     // with working sets, medium rows up to MQ_WS_MAX_ROW entries are
     // screened / fully solved above; the leading (longest) nmed_long stay here

@@ -303,6 +303,7 @@ class PdhcgEngine:
                 self.pl_x = torch.zeros(nl * C, **f64)
                 self.pl_col = torch.zeros(nl * C, dtype=torch.int32, device=dev)
                 self.pl_pos = torch.zeros(nl * C, dtype=torch.int32, device=dev)
+                self.pl_list = torch.zeros(nl, dtype=torch.int32, device=dev)
             # medium rows longer than WS_MAX_ROW (the leading nmed_long of
             # dm.med_rows): a pool of MED_CAP entries each
             nml = int(dm.struct.nmed_long) if dm.struct.nmed else 0
@@ -380,7 +381,7 @@ class PdhcgEngine:
                          "drift", "ws_lvl"):
                 setattr(s, name, getattr(self, name).data_ptr())
             if self.pool:
-                for name in ("pl_hdr", "pl_u", "pl_x", "pl_col", "pl_pos"):
+                for name in ("pl_hdr", "pl_u", "pl_x", "pl_col", "pl_pos", "pl_list"):
                     setattr(s, name, getattr(self, name).data_ptr())
             if self.mpool:
                 for name in ("pm_hdr", "pm_u", "pm_x", "pm_col", "pm_pos"):

@@ -24,7 +24,7 @@ def test_native_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(lib, name)
-    assert lib.mq_abi_version() == 11
+    assert lib.mq_abi_version() == 12
     # the ctypes mirrors have the C layout
     assert lib.mq_market_bytes() == ctypes.sizeof(_native.MqMarket)
     assert lib.mq_state_bytes() == ctypes.sizeof(_native.MqState)
