@@ -187,3 +187,28 @@ def test_medium_rows_solve_over_working_set_pools():
     assert hdr.shape[0] == nml and (hdr[:, 0] >= 0).mean() > 0.8
     _check_pools(ws, ws.dm.med_rows[:nml].cpu().numpy(), hdr, ws.pm_u, ws.pm_x, ws.pm_col,
                  ws.pm_pos, nat.MED_CAP)
+
+
+def test_working_set_levels_move_with_failures_and_rebuilds():
+    """Per-row width levels (mq_state.ws_lvl): every row starts at level 0; a
+    failed certificate widens its row's set by one level (some rows climb
+    over a few chunks of moving prices), levels stay in 0..3, and a rebuild
+    of every set (after the host writes the iterate) narrows each row by one
+    level.  The iterates are the unscreened ones (the tests above)."""
+    import torch
+
+    ws, _ = _pair(dict(n=40_000, m=4_000, q=0.025, seed=5), steps=(0.2, 0.2))
+    assert int(ws.ws_lvl.max()) == 0
+    for _ in range(6):
+        ws.run_chunk(40)
+    lv = ws.ws_lvl[:ws.dm.n].to(torch.int64)
+    assert int(lv.max()) <= 3 and int((lv > 0).sum()) > 0
+    before = lv.clone()
+    ws.restart()  # host writes x, p: every working set is rebuilt next iteration
+    ws.run_chunk(1)
+    after = ws.ws_lvl[:ws.dm.n].to(torch.int64)
+    # the rebuild iteration (the tile kernel) narrows every tile row one
+    # level; rows it does not rebuild (over 128 entries) keep theirs
+    assert bool((after <= before).all())
+    assert bool((after >= (before - 1).clamp(min=0)).all())
+    assert int((after < before).sum()) > 0
