@@ -473,7 +473,7 @@ def main():
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "iter/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t_ms / a.steps, 4),
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "higher_is_better": True, "scaling": "strong",  # one fixed market at every N
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"BASELINE config {a.config[1]}: {CONFIG_TEXT[a.config]}",
                    "n_buyers": n_full, "m_goods": m, "nnz": nnz_full, "seed": a.seed,
@@ -608,7 +608,7 @@ def reference_arm(a, rank, world):
         "metric": METRIC, "value": round(rate, 6), "unit": "iter/s", "n_gpus": world,
         "steps": steps, "warmup": warm, "ms_per_step": round(1e3 * total / steps, 3),
         "steps_requested": a.steps, "warmup_requested": a.warmup,
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "higher_is_better": True, "scaling": "strong",  # one fixed market at every N
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": f"BASELINE config {a.config[1]}: {CONFIG_TEXT[a.config]}",
                    "n_buyers": n, "m_goods": m, "nnz": nnz, "seed": a.seed,
