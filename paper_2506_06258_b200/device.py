@@ -72,11 +72,13 @@ def build_tiles(row_ptr, tile_entries=nat.TILE_ENTRIES, long_row=nat.LONG_ROW,
     nxt = torch.minimum(torch.minimum(j_e, rows + tile_rows), seg_end)
     nxt = torch.where(is_long, rows + 1, nxt)  # a long row is stepped over
     jump = torch.cat([nxt, torch.tensor([n], dtype=nxt.dtype, device=dev)])
-    starts = torch.zeros(1, dtype=torch.int64, device=dev)
+    # the orbit as a mask: after step k it holds the first 2^k tile starts
+    reach = torch.zeros(n + 1, dtype=torch.bool, device=dev)
+    reach[0] = True
     for _ in range(max(1, n.bit_length()) + 1):
-        starts = torch.unique(torch.cat([starts, jump[starts]]))
+        reach[jump[reach]] = True
         jump = jump[jump]
-    starts = starts[starts < n]
+    starts = torch.nonzero(reach[:n]).flatten()
     starts = starts[~is_long[starts]]
     tiles = torch.stack([starts, nxt[starts]], 1).contiguous()
     return tiles, long_rows
