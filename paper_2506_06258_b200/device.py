@@ -72,13 +72,11 @@ def build_tiles(row_ptr, tile_entries=nat.TILE_ENTRIES, long_row=nat.LONG_ROW,
     nxt = torch.minimum(torch.minimum(j_e, rows + tile_rows), seg_end)
     nxt = torch.where(is_long, rows + 1, nxt)  # a long row is stepped over
     jump = torch.cat([nxt, torch.tensor([n], dtype=nxt.dtype, device=dev)])
-    # the orbit as a mask: after step k it holds the first 2^k tile starts
-    reach = torch.zeros(n + 1, dtype=torch.bool, device=dev)
-    reach[0] = True
+    starts = torch.zeros(1, dtype=torch.int64, device=dev)
     for _ in range(max(1, n.bit_length()) + 1):
-        reach[jump[reach]] = True
+        starts = torch.unique(torch.cat([starts, jump[starts]]))
         jump = jump[jump]
-    starts = torch.nonzero(reach[:n]).flatten()
+    starts = starts[starts < n]
     starts = starts[~is_long[starts]]
     tiles = torch.stack([starts, nxt[starts]], 1).contiguous()
     return tiles, long_rows
