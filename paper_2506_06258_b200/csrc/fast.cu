@@ -419,9 +419,9 @@ __device__ __forceinline__ double row_root_warm(const double (&c)[PER], const do
 // entries: their prices have dropped by at most D (drift) since the working
 // set was built, so p_j s >= (p_j^ref - D) s >= theta (1 - D / P) s with
 // theta = min p^ref / u and P = min p^ref over them.  On C4 the working sets
-// hold ~5 % of the entries and the certificate holds for ~100 % of the rows
-// (tools/screen_stats.py, tools/ws_stats.py): one price gather in ~20 instead
-// of every entry's.
+// hold ~2.5 % of the entries and the certificate holds for all but ~1,600 of
+// the 10^7 rows per iteration (tools/ws_waste.py, tools/ws_stats.py): one
+// price gather in ~40 instead of every entry's.
 // The factor is per row (mq_state.ws_lvl): a row whose certificate failed
 // is rebuilt one level wider, a row with more working entries than slots one
 // level narrower, and every row one level narrower when all working sets
@@ -1836,8 +1836,8 @@ ws_kernel(const mq_market mk, const mq_state st, int it, int force_full) {
 }
 
 // Full solve of the listed rows (no working set, a failed certificate, more
-// than MQ_WS_SLOTS working entries, or x_prev_out requested), 16 lanes per row,
-// the row (<= MQ_REG_ROW entries) in registers, then the working set rebuilt:
+// than MQ_WS_SLOTS working entries, or x_prev_out requested), a warp per row,
+// the row (<= MQ_WS_MAX_ROW entries) in registers, then the working set rebuilt:
 // slots in ascending entry order, theta / P over the screened entries, C.
 #ifndef MQ_WSF_MINB
 #define MQ_WSF_MINB 2  // resident 256-thread CTAs per SM of the full solve
