@@ -40,6 +40,7 @@
 #include <math_constants.h>
 
 #include "mq_common.cuh"
+#include "mq_tma.cuh"
 
 // ---- compile-time configuration (tuning variants override with -D) ----
 #ifndef MQ_G
@@ -128,55 +129,6 @@ __device__ __forceinline__ Avg avg_weights(const int64_t *navg, int it) {
     return a;
 }
 
-// ------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_addr(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "MQ_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra MQ_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
-                                         uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar))
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes,
-                                              uint64_t *bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
-        : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
 // The fire-and-forget stores below carry no "memory" clobber: nothing in the
 // kernel reads these addresses after writing them, and without the compiler
 // barrier the loads around them (staged columns, utilities) can be scheduled
@@ -188,15 +140,6 @@ __device__ __forceinline__ void st_flag(uint8_t *p, bool v) {
 __device__ __forceinline__ void red_add_f64(double *p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v));
 }
-// 16-byte-aligned superset of [first, first+count) elements of size S
-template <int S>
-__device__ __forceinline__ void aligned_span(const void *base, int64_t first, int64_t count,
-                                             const unsigned char **src, uint32_t *bytes) {
-    const uint32_t d = (uint32_t)((first * S) & 15);
-    *src = reinterpret_cast<const unsigned char *>(base) + first * S - d;
-    *bytes = (uint32_t)((d + count * S + 15) & ~(int64_t)15);
-}
-
 // Column sums as fixed-point integers: x_e * cs_scale rounded to u64, added
 // with fire-and-forget atomics only for the entries with x_e > 0.  cs_scale =
 // 2^k is chosen per market so that no column can overflow while every x_e <
