@@ -424,6 +424,32 @@ __device__ __forceinline__ double drift_now(const mq_state &st) {
     return __dadd_ru(st.drift[0], st.drift[1]);
 }
 
+// Backoff of a pooled (medium / long) row, in its mq_state.ws_lvl byte
+// (unused by those rows otherwise): low 5 bits = iterations left to solve
+// the row in full without a pool (no screened attempt, no rebuild: the
+// pool is marked missing), high 3 bits = level L.  A failed certificate or
+// an overfull rebuild raises L (at most 5) and skips the next 2^L - 1
+// iterations; a passing certificate lowers L.  Where the pools do not pay
+// (prices oscillating in an exchange's late inner solves, or more working
+// entries than the pool holds) the attempt and the rebuild — which
+// re-gathers every entry's price — are overhead on top of the full solve.
+__device__ __forceinline__ bool pool_attempt(const mq_state &st, int64_t i) {
+    return !st.ws_lvl || (st.ws_lvl[i] & 31u) == 0;
+}
+__device__ __forceinline__ void pool_skipped(const mq_state &st, int64_t i) {
+    if (st.ws_lvl) st.ws_lvl[i] = (uint8_t)(st.ws_lvl[i] - 1u);  // countdown > 0
+}
+__device__ __forceinline__ void pool_outcome(const mq_state &st, int64_t i, bool pass) {
+    if (!st.ws_lvl) return;
+    int lv = st.ws_lvl[i] >> 5;
+    if (pass) {
+        if (lv) st.ws_lvl[i] = (uint8_t)((lv - 1) << 5);
+    } else {
+        lv = lv < 5 ? lv + 1 : 5;
+        st.ws_lvl[i] = (uint8_t)((lv << 5) | ((1 << lv) - 1));
+    }
+}
+
 // Rebuild row i's working set after its full solve (G lanes, entry t = lane
 // + G e in register e): the nonzero entries and the zero entries near the
 // threshold (p s < gamma w u) take slots in ascending entry order; theta =
@@ -886,6 +912,7 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
     uint8_t *s_f = lsm + L::kF;
     __shared__ double sm[192];
     __shared__ int64_t claimed;
+    __shared__ int s_attempt;  // the row's pool backoff, read once for the block
     __shared__ int wtot[T / 32 + 1];  // per-warp counts of a working-set rebuild chunk
     const double cnow = st.pl_hdr ? drift_now(st) : 0.0;
     int phase = 0;
@@ -896,7 +923,14 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
     constexpr int LB = MQ_LONG_LB;
     for (;;) {
         __syncthreads();  // the previous row's shared-memory reads are done
-        if (tid == 0) claimed = atomicAdd(st.blk_done + 1, 1);
+        if (tid == 0) {
+            claimed = atomicAdd(st.blk_done + 1, 1);
+            const int64_t nr = listed ? *(volatile int32_t *)(st.blk_done + 7) : mk.nlong;
+            s_attempt = claimed < nr
+                            ? (int)pool_attempt(st, mk.long_rows[listed ? (int64_t)st.pl_list[claimed]
+                                                                        : claimed])
+                            : 1;
+        }
         __syncthreads();
         // listed: only the rows primal_long_ws_kernel left (pool too large
         // for a warp, missing, or its certificate failed)
@@ -913,14 +947,20 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
         const double wi = mk.w[i];
         const double tw = tau * wi;
         double *__restrict__ gx = st.x + a;
+        bool failed_here = false;  // a screened attempt failed this iteration (block-uniform)
         // ---- screened solve over the row's working set (pool r): the same
         // certificate as the short rows'
         if (st.pl_hdr && !x_prev_out) {
             const int4 hd = reinterpret_cast<const int4 *>(st.pl_hdr)[r];
             const int h = hd.x;
             MQ_CHECK(h >= -2 && h <= CAP);
-            // a pool the warp pass could hold already failed there
-            if (h >= 0 && !(listed && h <= MQ_LONG_WCAP)) {
+            // a pool the warp pass could hold already failed there (or was
+            // skipped by its backoff, which this kernel applies itself to
+            // the larger pools)
+            // (the backoff countdown is the warp pass's to advance when listed)
+            const bool attempt = !(listed && h <= MQ_LONG_WCAP) && s_attempt;
+            if (h > 0 && attempt) failed_here = true;  // unless it passes below
+            if (h >= 0 && attempt) {
                 const int64_t po = r * (int64_t)CAP;
                 double s0w = 0.0, Aw = 0.0, Bw = 0.0;
                 for (int k = tid; k < h; k += T) {
@@ -996,9 +1036,11 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
                     if (tid == 0) {
                         my_sweeps += nsw;
                         st.srow[i] = sw;
+                        pool_outcome(st, i, true);
                     }
                     continue;  // the next row (the loop head syncs)
                 }
+                if (tid == 0 && h > 0) pool_outcome(st, i, false);
                 __syncthreads();  // the full solve below reuses the shared arrays
             }
         }
@@ -1100,7 +1142,13 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
             st.srow[i] = s;
         }
         const double inv_s = 1.0 / s;
-        if (st.pl_hdr) {
+        if (st.pl_hdr && (!s_attempt || failed_here)) {  // backing off: pool missing
+            if (tid == 0) {
+                if (!listed && !s_attempt) pool_skipped(st, i);
+                st.pl_hdr[4 * r] = -1;
+            }
+        }
+        if (st.pl_hdr && s_attempt && !failed_here) {
             // write-back fused with the working-set rebuild, chunk by chunk of
             // T entries so the block scan ranks working entries in ascending
             // position: nonzero entries and zero entries near the threshold
@@ -1171,6 +1219,7 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
                                             __float_as_int(__double2float_rd(pmn)),
                                             __float_as_int(__double2float_rd(cnow)))
                                 : make_int4(-2, 0, 0, 0);
+                if (base > CAP) pool_outcome(st, i, false);
             }
             continue;
         }
@@ -1230,7 +1279,9 @@ primal_long_ws_kernel(const mq_market mk, const mq_state st, int it) {
         const int h = hd.x;
         MQ_CHECK(h >= -2 && h <= MQ_LONG_CAP);
         bool solved = false;
-        if (h > 0 && h <= MQ_LONG_WCAP) {  // warp-uniform
+        const bool attempt = __shfl_sync(MQ_FULL, (int)pool_attempt(st, i), 0) != 0;
+        if (!attempt && lane == 0) pool_skipped(st, i);
+        if (attempt && h > 0 && h <= MQ_LONG_WCAP) {  // warp-uniform
             const int64_t po = r * (int64_t)MQ_LONG_CAP;
             double c[PC], u[PC], xk[PC];
             int jc[PC], ps[PC];
@@ -1269,8 +1320,11 @@ primal_long_ws_kernel(const mq_market mk, const mq_state st, int it) {
                 if (lane == 0) {
                     st.srow[i] = sw;
                     my_sweeps += nsw;
+                    pool_outcome(st, i, true);
                 }
                 solved = true;
+            } else if (lane == 0) {
+                pool_outcome(st, i, false);
             }
         }
         if (!solved && lane == 0) st.pl_list[atomicAdd(st.blk_done + 7, 1)] = r;
@@ -1318,7 +1372,15 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
         // rows longer than MQ_WS_MAX_ROW have a pool (the leading nmed_long)
         const bool pooled = st.pm_hdr != nullptr && r < mk.nmed_long;
         const int64_t po = r * (int64_t)MQ_MED_CAP;
-        if (pooled && !x_prev_out) {
+        const bool fresh =  // lane 0's read for the whole warp (lane 0 writes it below)
+            __shfl_sync(MQ_FULL, (int)(pooled && pool_attempt(st, i)), 0) != 0;
+        const bool attempt = fresh && !x_prev_out;
+        if (pooled && !fresh && lane == 0) {  // backing off: solved in full, pool missing
+            pool_skipped(st, i);
+            st.pm_hdr[4 * r] = -1;
+        }
+        bool failed = false;  // this iteration's certificate failed: back off now
+        if (attempt) {
             // screened solve over the pool, in registers; the certificate of
             // the short rows
             const int4 hd = reinterpret_cast<const int4 *>(st.pm_hdr)[r];
@@ -1362,11 +1424,15 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
                     if (lane == 0) {
                         st.srow[i] = sw;
                         my_sweeps += nsw;
+                        pool_outcome(st, i, true);
                     }
                     continue;
                 }
+                if (lane == 0) pool_outcome(st, i, false);
+                failed = true;
             }
         }
+        if (failed && lane == 0) st.pm_hdr[4 * r] = -1;  // no rebuild while backing off
         double s0p = 0.0, ap = 0.0, bp = 0.0;
         for (int t0 = lane; t0 < len; t0 += LB * G) {
             double pv[LB], xv[LB], uv[LB];
@@ -1403,7 +1469,7 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
             if (!ok) ++my_faults;
         }
         const double inv_s = 1.0 / sr;
-        if (pooled) {
+        if (pooled && fresh && !failed) {
             // write-back fused with the pool rebuild: warp-wide chunks of 32
             // entries in ascending position, ballots rank the working entries
             // (nonzero, or zero with p_j s < gamma w u_j)
@@ -1452,12 +1518,14 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
             double th = bp == CUDART_INF ? CUDART_INF : __ddiv_rd(bp, bu) * (1.0 - 4e-16);
             th = group_min<32>(th);
             pmn = group_min<32>(pmn);
-            if (lane == 0)
+            if (lane == 0) {
                 reinterpret_cast<int4 *>(st.pm_hdr)[r] =
                     base <= MQ_MED_CAP ? make_int4(base, __float_as_int(__double2float_rd(th)),
                                                    __float_as_int(__double2float_rd(pmn)),
                                                    __float_as_int(__double2float_rd(cnow)))
                                        : make_int4(-2, 0, 0, 0);
+                if (base > MQ_MED_CAP) pool_outcome(st, i, false);
+            }
             continue;
         }
         for (int t0 = lane; t0 < len; t0 += LB * G) {

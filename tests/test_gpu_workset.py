@@ -184,7 +184,12 @@ def test_medium_rows_solve_over_working_set_pools():
     ws.run_chunk(3)
     torch.cuda.synchronize()
     hdr = ws.pm_hdr.cpu().numpy()
-    assert hdr.shape[0] == nml and (hdr[:, 0] >= 0).mean() > 0.8
+    # rows whose certificate failed may be backing off (no pool for a few
+    # iterations, ws_lvl countdown > 0)
+    lv = ws.ws_lvl[ws.dm.med_rows[:nml].to(torch.int64)].cpu().numpy()
+    assert hdr.shape[0] == nml and (hdr[:, 0] >= 0).mean() > 0.6
+    assert np.all((hdr[:, 0] >= 0) | (hdr[:, 0] == -1) | (hdr[:, 0] == -2))
+    assert np.all(hdr[lv & 31 > 0, 0] == -1)  # a row backing off has no pool
     _check_pools(ws, ws.dm.med_rows[:nml].cpu().numpy(), hdr, ws.pm_u, ws.pm_x, ws.pm_col,
                  ws.pm_pos, nat.MED_CAP)
 
