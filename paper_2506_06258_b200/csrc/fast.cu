@@ -445,7 +445,10 @@ __device__ __forceinline__ void pool_outcome(const mq_state &st, int64_t i, bool
     if (pass) {
         if (lv) st.ws_lvl[i] = (uint8_t)((lv - 1) << 5);
     } else {
-        lv = lv < 5 ? lv + 1 : 5;
+#ifndef MQ_POOL_LSTEP
+#define MQ_POOL_LSTEP 1
+#endif
+        lv = lv + MQ_POOL_LSTEP < 5 ? lv + MQ_POOL_LSTEP : 5;
         st.ws_lvl[i] = (uint8_t)((lv << 5) | ((1 << lv) - 1));
     }
 }
