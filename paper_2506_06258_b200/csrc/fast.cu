@@ -439,18 +439,22 @@ __device__ __forceinline__ bool pool_attempt(const mq_state &st, int64_t i) {
 __device__ __forceinline__ void pool_skipped(const mq_state &st, int64_t i) {
     if (st.ws_lvl) st.ws_lvl[i] = (uint8_t)(st.ws_lvl[i] - 1u);  // countdown > 0
 }
-__device__ __forceinline__ void pool_outcome(const mq_state &st, int64_t i, bool pass) {
-    if (!st.ws_lvl) return;
+// returns the iterations the row now skips (0: rebuild at once, as before
+// any backoff: a first failure costs nothing extra)
+__device__ __forceinline__ int pool_outcome(const mq_state &st, int64_t i, bool pass) {
+    if (!st.ws_lvl) return 0;
     int lv = st.ws_lvl[i] >> 5;
     if (pass) {
         if (lv) st.ws_lvl[i] = (uint8_t)((lv - 1) << 5);
-    } else {
+        return 0;
+    }
 #ifndef MQ_POOL_LSTEP
 #define MQ_POOL_LSTEP 1
 #endif
-        lv = lv + MQ_POOL_LSTEP < 5 ? lv + MQ_POOL_LSTEP : 5;
-        st.ws_lvl[i] = (uint8_t)((lv << 5) | ((1 << lv) - 1));
-    }
+    lv = lv + MQ_POOL_LSTEP < 6 ? lv + MQ_POOL_LSTEP : 6;
+    const int skip = lv > 1 ? (1 << (lv - 1)) - 1 : 0;  // 0, 1, 3, 7, 15, 31
+    st.ws_lvl[i] = (uint8_t)((lv << 5) | skip);
+    return skip;
 }
 
 // Rebuild row i's working set after its full solve (G lanes, entry t = lane
@@ -916,6 +920,7 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
     __shared__ double sm[192];
     __shared__ int64_t claimed;
     __shared__ int s_attempt;  // the row's pool backoff, read once for the block
+    __shared__ int s_skip;     // the iterations a failed attempt now skips
     __shared__ int wtot[T / 32 + 1];  // per-warp counts of a working-set rebuild chunk
     const double cnow = st.pl_hdr ? drift_now(st) : 0.0;
     int phase = 0;
@@ -962,7 +967,6 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
             // the larger pools)
             // (the backoff countdown is the warp pass's to advance when listed)
             const bool attempt = !(listed && h <= MQ_LONG_WCAP) && s_attempt;
-            if (h > 0 && attempt) failed_here = true;  // unless it passes below
             if (h >= 0 && attempt) {
                 const int64_t po = r * (int64_t)CAP;
                 double s0w = 0.0, Aw = 0.0, Bw = 0.0;
@@ -1043,8 +1047,9 @@ primal_long_kernel(const mq_market mk, const mq_state st, int it, double *__rest
                     }
                     continue;  // the next row (the loop head syncs)
                 }
-                if (tid == 0 && h > 0) pool_outcome(st, i, false);
+                if (tid == 0) s_skip = h > 0 ? pool_outcome(st, i, false) : 0;
                 __syncthreads();  // the full solve below reuses the shared arrays
+                failed_here = s_skip > 0;  // backing off from now on (block-uniform)
             }
         }
         double s0 = 0.0, A = 0.0, B = 0.0;
@@ -1431,8 +1436,9 @@ primal_med_kernel(const mq_market mk, const mq_state st, int it, double *__restr
                     }
                     continue;
                 }
-                if (lane == 0) pool_outcome(st, i, false);
-                failed = true;
+                int skip = 0;
+                if (lane == 0) skip = pool_outcome(st, i, false);
+                failed = __shfl_sync(MQ_FULL, skip, 0) > 0;  // backing off from now on
             }
         }
         if (failed && lane == 0) st.pm_hdr[4 * r] = -1;  // no rebuild while backing off
